@@ -1,0 +1,45 @@
+// hshard-b200: graph-switch parameter redistribution.
+//
+// The reference specifies diff_strategies / plan_switch / apply_switch only in
+// prose; there is no reference code.  Planning here is the
+// SPEC's recipe on the reference primitives: build_table per changed
+// parameter (bsr.hpp:50) then one global fuse() (bsr.hpp:96).  Execution is
+// in hshard/exec.hpp.
+#pragma once
+
+#include "hshard/bsr.hpp"
+
+namespace hshard {
+
+// One parameter whose annotation changes (SPEC.md:413-418 output element).
+struct SwitchEntry {
+  int tensor_id = 0;
+  HetAnnotation src;
+  HetAnnotation dst;
+  Shape shape;
+};
+
+// A parameter's layout under two strategies (the CompGraph that would supply
+// these per-strategy slots is outside the resharding path).
+struct ParamLayouts {
+  int tensor_id = 0;
+  Shape shape;
+  HetAnnotation a;
+  HetAnnotation b;
+};
+
+// Changed parameters only; annotations_equal pairs are omitted.
+std::vector<SwitchEntry> diff_strategies(const std::vector<ParamLayouts>& params);
+
+struct SwitchPlan {
+  std::vector<SwitchEntry> diff;  // tensor order of the plan
+  DType dtype = DType::F32;
+  BsrPlan plan;                   // fused: one fusion group per (sender, receiver)
+};
+
+// build_table per entry (elem bytes = dtype width), then fuse.
+// Throws PartialUnderBsr for Partial parameters.
+SwitchPlan plan_switch(const std::vector<SwitchEntry>& diff, DType dtype,
+                       const Bandwidth& bandwidth = Bandwidth::uniform());
+
+}  // namespace hshard

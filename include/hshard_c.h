@@ -1,0 +1,141 @@
+/* hshard-b200 C ABI — the drop-in boundary of the HSPMD resharding path.
+ *
+ * The reference (Hetu v2 hshard, /root/reference/proj) is a C++20 library with
+ * no FFI; its path is the C++ API in include/hshard (which this library
+ * also exports, unchanged).  This header is the thin C layer any host
+ * language binds (ctypes / cgo / JNI — see INTEGRATION.md):
+ *   - plain pointers, sizes and NUL-terminated strings only;
+ *   - annotations cross the boundary in the reference's own text form,
+ *     HetAnnotation::str() (reference annotation.cpp:146-170), e.g.
+ *       "hsize=2 hdim=0 [(0,1){-1:2}; (2,3){-1:2}] ratios=3/4,1/4";
+ *   - every call returns 0 on success or 1 + hshard::Errc on failure
+ *     (reference common.hpp:34-70 order; executor codes appended), with a
+ *     thread-local message in hs_last_error();
+ *   - strings returned through `char**` are malloc'd; release with hs_free.
+ *
+ * Each entry point names the reference interface it replaces. */
+#ifndef HSHARD_C_H_
+#define HSHARD_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype codes = hshard::DType ordinals (reference common.hpp:28 + BF16). */
+enum { HS_F32 = 0, HS_F64 = 1, HS_I32 = 2, HS_I64 = 3, HS_BF16 = 4 };
+
+const char* hs_last_error(void);
+const char* hs_errc_name(int errc);           /* reference errc_name, common.cpp:50 */
+void hs_free(void* p);
+int hs_version(void);
+
+/* ---------------------------------------------------------------- planner */
+typedef struct hs_plan hs_plan; /* a CommPlan, or a fused switch BsrPlan */
+
+/* classify(src, dst, shape, dtype, bandwidth)          reference resolve.hpp:95-97
+ * bw: "u" (Bandwidth::uniform()) or "d=<w>;a-b=<w>;..." (Bandwidth::set). */
+int hs_classify(const char* src, const char* dst, const int64_t* shape, int ndim, int dtype,
+                const char* bw, hs_plan** out);
+
+/* plan_switch(diff, shapes, bandwidth): build_table per changed tensor, then
+ * fuse()                                   SPEC.md:419-427; reference bsr.hpp:50,96
+ * shapes_flat holds ndims[i] extents per tensor, concatenated. */
+int hs_plan_switch(int n, const int* tensor_ids, const char* const* src, const char* const* dst,
+                   const int64_t* shapes_flat, const int* ndims, int dtype, const char* bw,
+                   hs_plan** out);
+
+/* Canonical JSON of the plan (byte-identical to oracle/ref_tool's dump of the
+ * reference planner's CommPlan / BsrPlan). */
+int hs_plan_dump(const hs_plan* plan, char** json);
+void hs_plan_destroy(hs_plan* plan);
+
+/* build_table(...) dump                                reference bsr.hpp:50-51 */
+int hs_build_table(const char* src, const char* dst, const int64_t* shape, int ndim,
+                   int tensor_id, int elem_bytes, char** json);
+/* make_plan / make_plan_naive over build_table          reference bsr.hpp:92,100 */
+int hs_make_plan(const char* src, const char* dst, const int64_t* shape, int ndim,
+                 int elem_bytes, const char* bw, int naive, char** json);
+
+/* placement(anno, shape, device)                  reference annotation.hpp:131
+ * lo/hi receive ndim bounds; ord receives {partial_index, partial_count,
+ * replica_index, replica_count}. */
+int hs_placement(const char* anno, const int64_t* shape, int ndim, int device, int64_t* lo,
+                 int64_t* hi, int* ord);
+/* convert_hsize                                    reference annotation.hpp:133 */
+int hs_convert_hsize(const char* anno, int target, char** out);
+/* annotations_equal -> *eq                          reference annotation.hpp:134 */
+int hs_annotations_equal(const char* a, const char* b, int* eq);
+/* validate -> JSON list of Errc names              reference annotation.hpp:124 */
+int hs_validate(const char* anno, const int64_t* shape, int ndim, char** json);
+/* align_shard_specs -> JSON [[key_a,key_b,count],...] or null
+ *                                                  reference annotation.hpp:143 */
+int hs_align_shard_specs(const char* a, const char* b, char** json);
+
+/* ---------------------------------------------------------------- executor
+ * The reference declares execute_plan (sim.hpp:77-79) but never defines it;
+ * this is its B200 implementation.  One hs_ctx per process; one process per
+ * GPU ("rank").  Virtual device v of a plan lives on rank v_to_rank[v]. */
+typedef struct hs_ctx hs_ctx;
+typedef struct hs_prog hs_prog;
+
+/* Creates the per-GPU context: binds `gpu`, allocates a symmetric arena of
+ * `arena_bytes` of HBM (all shards, intermediates and staging live in it) and
+ * a flag block for cross-rank barriers. */
+int hs_ctx_create(int rank, int world, int gpu, size_t arena_bytes, hs_ctx** out);
+void hs_ctx_destroy(hs_ctx* ctx);
+/* Base device pointer of this rank's arena. */
+int hs_ctx_arena(hs_ctx* ctx, void** base, size_t* bytes);
+/* IPC handles of this rank's arena/flags (2 x 64 bytes) for peers to open. */
+int hs_ctx_ipc_handle(hs_ctx* ctx, unsigned char* out128);
+/* Map every peer's arena (handles gathered by the host, rank-major,
+ * world x 128 bytes).  Enables peer access.  Call once, after create. */
+int hs_ctx_open_peers(hs_ctx* ctx, const unsigned char* all_handles);
+
+/* Bump allocator inside the arena: offsets are identical on every rank when
+ * every rank performs the same sequence of allocations (symmetric heap). */
+int hs_ctx_alloc(hs_ctx* ctx, size_t bytes, size_t* offset);
+int hs_ctx_reset_alloc(hs_ctx* ctx, size_t offset);
+
+/* Compile a plan for this rank.  v_to_rank maps virtual device id -> rank for
+ * ids [0, n_virt).  src_off / dst_off give, per virtual device id, the arena
+ * offset of that device's shard on its rank (row-major over its placement
+ * box; SIZE_MAX = not present).  Intermediate (mid) shards are allocated
+ * from the arena by the compiler (symmetrically). flags: HS_PROG_* bits. */
+enum { HS_PROG_FUSE_PHASES = 1, HS_PROG_NO_GRAPH = 2 };
+int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
+                    const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);
+void hs_prog_destroy(hs_prog* prog);
+/* Run on `stream` (cudaStream_t, NULL = the ctx stream).  Multi-rank programs
+ * include device-side barriers; every rank must call run. */
+int hs_prog_run(hs_prog* prog, void* stream);
+/* Host-buffer execution (reference-facing e2e path): H2D of this rank's
+ * source shards from host pointers (indexed by virtual id; NULL = skip),
+ * run, D2H of destination shards.  Synchronous. */
+int hs_prog_run_host(hs_prog* prog, const void* const* src_host, void* const* dst_host);
+/* JSON statistics: kernels per run, bytes (HBM read/write, NVLink in/out) per
+ * run for this rank, task counts. */
+int hs_prog_stats(const hs_prog* prog, char** json);
+
+/* Deterministic counter-hash payload, written
+ * into this rank's shard of virtual device `dev` for annotation `anno`. */
+int hs_fill_shard(hs_ctx* ctx, const char* anno, const int64_t* shape, int ndim, int dtype,
+                  int device, size_t offset, uint32_t seed, int tensor_id, int mode,
+                  void* stream);
+/* Count cells of the shard at `offset` that differ from the logical
+ * counter-hash tensor (grid mode; non-Partial annotations only). */
+int hs_verify_shard(hs_ctx* ctx, const char* anno, const int64_t* shape, int ndim, int dtype,
+                    int device, size_t offset, uint32_t seed, int tensor_id,
+                    unsigned long long* mismatches, void* stream);
+/* Copy `bytes` at arena `offset` to/from host (synchronous). */
+int hs_ctx_read(hs_ctx* ctx, size_t offset, void* host, size_t bytes);
+int hs_ctx_write(hs_ctx* ctx, size_t offset, const void* host, size_t bytes);
+int hs_ctx_sync(hs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSHARD_C_H_ */

@@ -1,0 +1,152 @@
+// hshard-b200 C ABI: planner entry points (include/hshard_c.h).
+#include <cstdlib>
+#include <cstring>
+#include <variant>
+
+#include "capi_common.hpp"
+#include "hshard/resolve.hpp"
+#include "hshard/switch.hpp"
+
+using namespace hshard;
+
+namespace hshard::capi {
+
+thread_local std::string g_last_error;
+
+int fail_code(Errc e, const std::string& msg) {
+  g_last_error = msg;
+  return 1 + static_cast<int>(e);
+}
+
+char* dup_string(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+Shape to_shape(const int64_t* shape, int ndim) {
+  if (ndim < 0 || (ndim > 0 && !shape)) fail(Errc::ShapeMismatch, "bad shape");
+  return Shape(shape, shape + ndim);
+}
+
+DType to_dtype(int code) {
+  if (code < 0 || code > static_cast<int>(DType::BF16)) fail(Errc::ParseError, "bad dtype code");
+  return static_cast<DType>(code);
+}
+
+}  // namespace hshard::capi
+
+using namespace hshard::capi;
+
+extern "C" {
+
+const char* hs_last_error(void) { return g_last_error.c_str(); }
+const char* hs_errc_name(int errc) { return errc_name(static_cast<Errc>(errc)); }
+void hs_free(void* p) { std::free(p); }
+int hs_version(void) { return 1; }
+
+int hs_classify(const char* src, const char* dst, const int64_t* shape, int ndim, int dtype,
+                const char* bw, hs_plan** out) {
+  return guarded([&] {
+    auto plan = std::make_unique<hs_plan>();
+    plan->comm = classify(parse_annotation(src), parse_annotation(dst), to_shape(shape, ndim),
+                          to_dtype(dtype), parse_bandwidth(bw ? bw : "u"));
+    *out = plan.release();
+  });
+}
+
+int hs_plan_switch(int n, const int* tensor_ids, const char* const* src, const char* const* dst,
+                   const int64_t* shapes_flat, const int* ndims, int dtype, const char* bw,
+                   hs_plan** out) {
+  return guarded([&] {
+    std::vector<SwitchEntry> diff;
+    const int64_t* cursor = shapes_flat;
+    for (int i = 0; i < n; ++i) {
+      SwitchEntry e;
+      e.tensor_id = tensor_ids[i];
+      e.src = parse_annotation(src[i]);
+      e.dst = parse_annotation(dst[i]);
+      e.shape = to_shape(cursor, ndims[i]);
+      cursor += ndims[i];
+      diff.push_back(std::move(e));
+    }
+    auto plan = std::make_unique<hs_plan>();
+    plan->sw = plan_switch(diff, to_dtype(dtype), parse_bandwidth(bw ? bw : "u"));
+    *out = plan.release();
+  });
+}
+
+int hs_plan_dump(const hs_plan* plan, char** json) {
+  return guarded([&] {
+    *json = dup_string(plan->comm ? dump_plan(*plan->comm) : dump_bsr(plan->sw->plan));
+  });
+}
+
+void hs_plan_destroy(hs_plan* plan) { delete plan; }
+
+int hs_build_table(const char* src, const char* dst, const int64_t* shape, int ndim,
+                   int tensor_id, int elem_bytes, char** json) {
+  return guarded([&] {
+    *json = dup_string(dump_table(build_table(parse_annotation(src), parse_annotation(dst),
+                                              to_shape(shape, ndim), tensor_id, elem_bytes)));
+  });
+}
+
+int hs_make_plan(const char* src, const char* dst, const int64_t* shape, int ndim,
+                 int elem_bytes, const char* bw, int naive, char** json) {
+  return guarded([&] {
+    const BsrTable t =
+        build_table(parse_annotation(src), parse_annotation(dst), to_shape(shape, ndim), 0, elem_bytes);
+    *json = dup_string(dump_bsr(naive ? make_plan_naive(t) : make_plan(t, parse_bandwidth(bw ? bw : "u"))));
+  });
+}
+
+int hs_placement(const char* anno, const int64_t* shape, int ndim, int device, int64_t* lo,
+                 int64_t* hi, int* ord) {
+  return guarded([&] {
+    const SliceRegion r = placement(parse_annotation(anno), to_shape(shape, ndim), device);
+    for (int d = 0; d < ndim; ++d) {
+      lo[d] = r.bounds[d][0];
+      hi[d] = r.bounds[d][1];
+    }
+    ord[0] = r.partial_index;
+    ord[1] = r.partial_count;
+    ord[2] = r.replica_index;
+    ord[3] = r.replica_count;
+  });
+}
+
+int hs_convert_hsize(const char* anno, int target, char** out) {
+  return guarded([&] { *out = dup_string(convert_hsize(parse_annotation(anno), target).str()); });
+}
+
+int hs_annotations_equal(const char* a, const char* b, int* eq) {
+  return guarded([&] { *eq = annotations_equal(parse_annotation(a), parse_annotation(b)) ? 1 : 0; });
+}
+
+int hs_validate(const char* anno, const int64_t* shape, int ndim, char** json) {
+  return guarded([&] {
+    std::string s = "[";
+    const auto issues = validate(parse_annotation(anno), to_shape(shape, ndim));
+    for (size_t i = 0; i < issues.size(); ++i)
+      s += std::string(i ? "," : "") + "\"" + errc_name(issues[i].code) + "\"";
+    *json = dup_string(s + "]");
+  });
+}
+
+int hs_align_shard_specs(const char* a, const char* b, char** json) {
+  return guarded([&] {
+    const auto f = align_shard_specs(parse_shard_spec(a), parse_shard_spec(b));
+    if (!f) {
+      *json = dup_string("null");
+      return;
+    }
+    std::string s = "[";
+    for (size_t i = 0; i < f->size(); ++i)
+      s += std::string(i ? "," : "") + "[" + std::to_string((*f)[i].key_a) + "," +
+           std::to_string((*f)[i].key_b) + "," + std::to_string((*f)[i].count) + "]";
+    *json = dup_string(s + "]");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,35 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+if GOLDEN not in sys.path:
+    sys.path.insert(0, GOLDEN)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (run on the GPU box via gpurun)")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.fixture(scope="session")
+def gpu_ctx():
+    """One executor context on cuda:0 for the whole GPU test session."""
+    if not cuda_available():
+        pytest.skip("no GPU")
+    from paper_2504_20490_b200 import executor
+    ctx = executor.Context(arena_bytes=int(os.environ.get("HS_TEST_ARENA_GB", "40")) << 30)
+    yield ctx
+    ctx.close()
