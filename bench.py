@@ -1,0 +1,433 @@
+#!/usr/bin/env python3
+"""hshard-b200 benchmark: resharding GB/s and graph-switch latency on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2e] [--impl ours|reference]
+
+One "step" = one execution of the compiled resharding plan of the workload
+(BASELINE.json configs; default configs[1] = cfg2e, the Partial->Split(1)
+hierarchical reduce-scatter of 8192x8192 bf16 over the DS union {TP4, TP2+TP2},
+8 virtual devices mapped block-wise onto the N GPUs).  Inputs (1 GiB of
+partial sums per step) exceed the 126 MB L2, so no flush is needed.
+
+value    = whole-job destination-resident bytes / device time per step (GB/s),
+           timed with CUDA events on the launching stream, max over ranks.
+e2e      = the same metric through the C-ABI host-buffer path
+           (hs_prog_run_host: H2D of this rank's source shards from pinned
+           memory, the plan, D2H of its destination shards) -- the headline.
+roofline = the dominant kernel (the plan phase with the largest share of the
+           step), algorithmic bytes per launch / its event-timed duration vs the
+           measured HBM copy peak (N=1) or NVLink (N>1, per direction).
+cpu_baseline (rank 0, N=1) = the reference planner + the reference's own
+           per-cell Tensor primitives (oracle/_ref/ref_tool, command X) on a
+           bounded row-sample of the same workload, all host threads.
+--impl reference = that CPU path alone, as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+METRIC = "resharding GB/s and graph-switch latency (ms) at 1/2/4/8 B200 vs roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="cfg2e")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-switch", action="store_true", help="skip the cfg4 graph-switch probe")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--fuse", action="store_true", help="compile with HS_PROG_FUSE_PHASES")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def ncu_traffic(workload: str, phase: int):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"{workload}/phase{phase}")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------- cpu / reference
+def sample_transition(w, rows_cap: int):
+    """Bounded sample of a classify workload: the first dim cut to rows_cap."""
+    tid, src, dst, shape = w.transitions[0]
+    shape = list(shape)
+    if shape[0] > rows_cap:
+        shape[0] = rows_cap
+    return src, dst, shape
+
+
+def run_ref_tool(w, rows_cap: int, reps: int, warmup: int, threads: int):
+    src, dst, shape = sample_transition(w, rows_cap)
+    dt = "f32" if w.dtype == "bf16" else w.dtype  # reference DType has no bf16
+    cmd = f"X|{dt}|{','.join(map(str, shape))}|u|{src}|{dst}|1|grid|{reps}|0|{threads}|{warmup}\n"
+    out = subprocess.run([REF_TOOL], input=cmd, capture_output=True, text=True, timeout=3600)
+    j = json.loads(out.stdout.strip().splitlines()[-1])
+    if "error" in j:
+        raise RuntimeError(j)
+    from paper_2504_20490_b200 import hshard as H
+    # dst-resident bytes of the sample in the workload's dtype
+    es = H.DTYPE_BYTES[w.dtype]
+    dst_bytes = j["dst_bytes"] // H.DTYPE_BYTES[dt] * es
+    return {"seconds": j["mean"], "best": j["seconds"], "dst_bytes": dst_bytes, "shape": shape,
+            "threads": j["threads"]}
+
+
+def cpu_baseline(w, rows_cap=1024, reps=3, warmup=1):
+    threads = os.cpu_count() or 1
+    if os.path.exists(REF_TOOL) and w.kind == "classify":
+        r = run_ref_tool(w, rows_cap, reps, warmup, threads)
+        return {"value": r["dst_bytes"] / r["seconds"] / 1e9, "unit": "GB/s", "cores": r["threads"],
+                "kind": "reference",
+                "sample": (f"{w.name} rows cut to {r['shape'][0]} (shape {r['shape']}), mean of "
+                           f"{reps} runs after {warmup} warm-up; reference classify + reference "
+                           "Tensor::slice/write_slice/add_slice (tensor.cpp:84-114) driven per "
+                           "SPEC.md:467-495 by oracle/ref_tool.cpp, split by target device over "
+                           f"{r['threads']} threads; doubles per cell (tensor.hpp:24)")}
+    # numpy oracle port (switch workloads, or no reference build)
+    import numpy as np
+    from oracle import executor as ox
+    from paper_2504_20490_b200 import hshard as H
+    if w.kind == "classify":
+        src, dst, shape = sample_transition(w, rows_cap)
+        plan = H.classify(src, dst, shape, w.dtype).json()
+        shards = ox.scatter(src, shape, w.dtype, 1)
+        t0 = time.perf_counter()
+        out = ox.execute_plan(plan, shards, w.dtype)
+        sec = time.perf_counter() - t0
+        nbytes = sum(a.nbytes for a in out.values())
+        sample = f"{w.name} rows cut to {shape[0]}, numpy oracle port (oracle/executor.py)"
+    else:
+        entries = [e for e in w.transitions if len(e[3]) == 2][:12]
+        plan = H.plan_switch(entries, w.dtype).json()
+        src = {}
+        for tid, s, d, shp in entries:
+            for dev, a in ox.scatter(s, shp, w.dtype, 1, tid).items():
+                src[(tid, dev)] = a
+        t0 = time.perf_counter()
+        out = ox.execute_switch(plan, entries, src, w.dtype)
+        sec = time.perf_counter() - t0
+        nbytes = sum(a.nbytes for a in out.values())
+        sample = f"{w.name}: first {len(entries)} 2-d parameters, numpy oracle port"
+    return {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": sample}
+
+
+def reference_arm(args, w, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    if os.path.exists(REF_TOOL) and w.kind == "classify":
+        r = run_ref_tool(w, 512, max(1, args.steps), max(3, args.warmup) if args.warmup else 0,
+                         threads)
+        value = r["dst_bytes"] / r["seconds"] / 1e9
+        cb = {"value": value, "unit": "GB/s", "cores": r["threads"], "kind": "reference",
+              "sample": (f"{w.name} rows cut to {r['shape'][0]} per step; reference classify + "
+                         "reference Tensor primitives (oracle/ref_tool X), "
+                         f"{r['threads']} threads")}
+        ms = r["seconds"] * 1e3
+    else:
+        cb = cpu_baseline(w)
+        value, ms = cb["value"], None
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
+            "data": "synthetic (counter-hash grid payload)",
+            "config": {"workload": w.name, "sample": cb["sample"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_2504_20490_b200 import workloads as W
+    w = W.by_name(args.config)
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(backend="cpu:gloo,cuda:nccl")
+    if args.impl == "reference":
+        reference_arm(args, w, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+    from paper_2504_20490_b200 import hshard as H
+    from paper_2504_20490_b200.executor import HS_PROG_FUSE_PHASES, Context, Program, ShardLayout
+
+    torch.cuda.set_device(local)
+    free, _ = torch.cuda.mem_get_info(local)
+    arena = max(8 << 30, free - (10 << 30))
+    ctx = Context(arena, rank=rank, world=world, gpu=local)
+
+    def allreduce_max(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def build(work):
+        if work.kind == "classify":
+            tid, s, d, shp = work.transitions[0]
+            plan = H.classify(s, d, shp, work.dtype)
+        else:
+            plan = H.plan_switch(work.transitions, work.dtype)
+        lay = ShardLayout(ctx, plan, work.n_virtual)
+        prog = Program(ctx, plan, lay, HS_PROG_FUSE_PHASES if args.fuse else 0)
+        return plan, lay, prog
+
+    stream = torch.cuda.Stream(device=local)
+    sp = stream.cuda_stream
+
+    def timed(prog, steps, warmup, profile=False):
+        for _ in range(warmup):
+            prog.run(sp)
+        stream.synchronize()
+        ctx.sync()
+        barrier()
+        if profile:
+            prog.profile(True)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record()
+            for _ in range(steps):
+                prog.run(sp)
+            b.record()
+        b.synchronize()
+        ctx.sync()
+        barrier()
+        ms = a.elapsed_time(b) / steps
+        phase = None
+        if profile:
+            phase, runs = prog.phase_ms()
+            phase = [x / max(1, runs) for x in phase]
+            prog.profile(False)
+        return allreduce_max(ms), phase
+
+    # ---- headline workload
+    plan, lay, prog = build(w)
+    st = prog.stats()
+    lay.fill_src(1, "grid", sp)
+    stream.synchronize()
+    prog.run(sp)
+    stream.synchronize()
+    ctx.sync()
+    dst_has_partial = any(r["partial"][1] > 1 for r in lay.dst.values())
+    verified = None
+    if not dst_has_partial:
+        bad = lay.verify_dst(1)
+        verified = bool(allreduce_max(float(bad)) == 0)
+    with ClockSampler(local) as clocks:
+        ms, phase_ms = timed(prog, args.steps, args.warmup, profile=True)
+    clk = clocks.summary()
+
+    total_dst = sum(r["bytes"] for r in lay.dst.values())
+    value = total_dst / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (phase) on this rank
+    peak, peak_kind = measured_peaks()
+    dom = max(range(len(phase_ms)), key=lambda p: phase_ms[p])
+    rd, wr, nvin = st["phase_bytes"][dom]
+    kern_s = phase_ms[dom] * 1e-3
+    if world == 1 or nvin == 0:
+        achieved = (rd + wr) / kern_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(w.name, dom),
+                "kernel": f"box_phase_kernel phase {dom} ({['bottom', 'top'][dom] if st['phases'] == 2 else 'plan'})",
+                "bytes_per_launch": rd + wr, "launch_ms": phase_ms[dom],
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "share_of_step": phase_ms[dom] / ms if ms else None}
+    else:
+        achieved = nvin / kern_s / 1e9
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_GBS, "unit": "GB/s",
+                "frac": achieved / NVLINK_GBS, "traffic": None,
+                "kernel": f"box_phase_kernel phase {dom}", "bytes_per_launch": nvin,
+                "launch_ms": phase_ms[dom], "hbm_achieved": (rd + wr) / kern_s / 1e9,
+                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)"}
+
+    # ---- e2e through the host-buffer C-ABI path (pinned host memory)
+    src_host, dst_host, keep = {}, {}, []
+    for key, rec in lay.local("src").items():
+        t = torch.empty(rec["bytes"], dtype=torch.uint8, pin_memory=True)
+        keep.append(t)
+        a = t.numpy().view(np.uint8)
+        a[:] = np.frombuffer(ctx.read(rec["offset"], rec["bytes"]), dtype=np.uint8)
+        src_host[key] = a
+    for key, rec in lay.local("dst").items():
+        t = torch.empty(rec["bytes"], dtype=torch.uint8, pin_memory=True)
+        keep.append(t)
+        dst_host[key] = t.numpy()
+    h2d = sum(a.nbytes for a in src_host.values())
+    d2h = sum(a.nbytes for a in dst_host.values())
+    prog.run_host(src_host, dst_host)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        prog.run_host(src_host, dst_host)
+    e2e_ms = allreduce_max((time.perf_counter() - t0) * 1e3 / args.e2e_steps)
+    barrier()
+    e2e = {"value": total_dst / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "path": "hs_prog_run_host (C ABI): pinned H2D of local src shards, plan, D2H of local dst shards"}
+    del prog, lay
+    ctx.reset(0)
+
+    # ---- graph-switch latency probe (cfg4, Llama-2-7B TP2xPP4 -> TP4xPP2)
+    switch = None
+    if not args.no_switch:
+        sw = W.config4()
+        if W.resident_bytes(sw) / world * 1.1 < ctx.arena_bytes:
+            splan, slay, sprog = build(sw)
+            slay.fill_src(2, "grid", sp)
+            stream.synchronize()
+            sms, sphase = timed(sprog, 10, 3)
+            sst = sprog.stats()
+            sbad = slay.verify_dst(2)
+            sdst = sum(r["bytes"] for r in slay.dst.values())
+            switch = {"workload": "cfg4 Llama-2-7B TP2xPP4->TP4xPP2 (291 params, 13.48 GB bf16)",
+                      "ms": sms, "GB/s": sdst / (sms * 1e-3) / 1e9,
+                      "transfer_bytes": sum(t[4] for t in splan.json()["xfer"]),
+                      "verified": bool(allreduce_max(float(sbad)) == 0),
+                      "hbm_bytes_rank0": sst["hbm_read"] + sst["hbm_write"],
+                      "hbm_frac": (sst["hbm_read"] + sst["hbm_write"]) / (sms * 1e-3) / 1e9 / peak}
+            del sprog, slay
+            ctx.reset(0)
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cb = cpu_baseline(w)
+        except Exception as e:  # reported, never fatal for the GPU number
+            cb = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                  "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": w.dtype, "data": "synthetic (counter-hash grid payload)",
+            "config": {"workload": w.name, "n_virtual": w.n_virtual,
+                       "virtual_to_gpu": "block (v // (8 / N))", "shape": list(w.transitions[0][3]),
+                       "plan": [s["kind"] for s in plan.json()["bottom"] + plan.json()["top"]]
+                       if w.kind == "classify" else "fused Bsr",
+                       "dst_resident_bytes": total_dst, "l2": "inputs larger than L2 (no flush)",
+                       "fuse_phases": bool(args.fuse)},
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": args.steps * st["kernels_per_run"],
+            "kernels_per_step": st["kernels_per_run"], "phase_ms": phase_ms,
+            "verified": verified, "clocks": clk, "graph_switch": switch,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,12 @@ int hs_prog_run(hs_prog* prog, void* stream);
  * source shards from host pointers (indexed by virtual id; NULL = skip),
  * run, D2H of destination shards.  Synchronous. */
 int hs_prog_run_host(hs_prog* prog, const void* const* src_host, void* const* dst_host);
+/* Per-phase kernel timing with CUDA events on the launching stream (bench /
+ * roofline evidence).  hs_prog_profile(1) resets and enables; every run then
+ * records 2 events per phase; hs_prog_phase_ms sums elapsed ms per phase over
+ * the profiled runs (synchronising) and reports the run count. */
+int hs_prog_profile(hs_prog* prog, int enable);
+int hs_prog_phase_ms(hs_prog* prog, double* out, int n, int* runs);
 /* JSON statistics: kernels per run, bytes (HBM read/write, NVLink in/out) per
  * run for this rank, task counts. */
 int hs_prog_stats(const hs_prog* prog, char** json);

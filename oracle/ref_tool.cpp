@@ -25,7 +25,8 @@
 //   Q|anno|anno                               annotations_equal
 //   A|ds|ds                                   align_shard_specs
 //   V|shape|anno                              validate (issue codes)
-//   X|dtype|shape|bw|src|dst|seed|mode|reps|emit   reference-primitive executor
+//   X|dtype|shape|bw|src|dst|seed|mode|reps|emit[|threads[|warmup]]
+//                                             reference-primitive executor
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -345,8 +346,11 @@ ShardMap init_target(const HetAnnotation& a, const Shape& shape, DType dt) {
 // Phase semantics per SURVEY Appendix C (restating SPEC.md:467-495) using the
 // reference's Tensor::slice / write_slice / add_slice.  Reductions use
 // ascending device id order; values are doubles (tensor.hpp:24).
+// Work is split by TARGET device across `nthreads` host threads (thread `tid`
+// owns targets d with d % nthreads == tid); targets are independent tensors.
 void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardMap& in,
-              ShardMap& out) {
+              ShardMap& out, int tid = 0, int nthreads = 1) {
+  auto owns = [&](DeviceId d) { return d % nthreads == tid; };
   auto piece = [&](DeviceId m, const SliceRegion& logical) {
     const auto& [reg, ten] = in.at(m);
     return ten.slice(local_box(reg, logical));
@@ -361,10 +365,11 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
   switch (step.kind) {
     case StepKind::Identity:
       for (DeviceId d : phase_src.dg_union.at(step.subgroup).devices)
-        out.at(d).second = in.at(d).second;
+        if (owns(d)) out.at(d).second = in.at(d).second;
       break;
     case StepKind::SendRecv:
-      for (auto [s, r] : step.pairs) out.at(r).second = in.at(s).second;
+      for (auto [s, r] : step.pairs)
+        if (owns(r)) out.at(r).second = in.at(s).second;
       break;
     case StepKind::AllReduce:
     case StepKind::ReduceScatter:
@@ -372,6 +377,7 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
         std::vector<DeviceId> order(grp.begin(), grp.end());
         std::sort(order.begin(), order.end());
         for (DeviceId d : grp) {
+          if (!owns(d)) continue;
           SliceRegion target = out.at(d).first;
           SliceRegion box;
           box.bounds = target.bounds;
@@ -389,6 +395,7 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
     case StepKind::AllGather:
       for (const auto& grp : step.groups) {
         for (DeviceId d : grp) {
+          if (!owns(d)) continue;
           SliceRegion target = out.at(d).first;
           int64_t covered = 0;
           for (DeviceId m : grp) {
@@ -406,6 +413,7 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
     case StepKind::SplitAllGather:
       for (const auto& sc : step.slices) {
         for (DeviceId r : sc.receivers) {
+          if (!owns(r)) continue;
           const SliceRegion& rr = out.at(r).first;
           std::vector<DeviceId> cs(sc.contributors.begin(), sc.contributors.end());
           std::sort(cs.begin(), cs.end());
@@ -424,27 +432,49 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
       }
       break;
     case StepKind::Bsr:
-      for (const auto& c : step.bsr->local_copies) put(c.device, c.region, piece(c.device, c.region), false);
+      for (const auto& c : step.bsr->local_copies)
+        if (owns(c.device)) put(c.device, c.region, piece(c.device, c.region), false);
       for (const auto& fg : step.bsr->fusion_groups)
         for (int i : fg.transfer_indices) {
           const auto& t = step.bsr->transfers[i];
-          put(t.receiver, t.region, piece(t.sender, t.region), false);
+          if (owns(t.receiver)) put(t.receiver, t.region, piece(t.sender, t.region), false);
         }
       break;
   }
 }
 
-ShardMap run_plan(const CommPlan& plan, const ShardMap& src, DType dt) {
+void run_phase(const std::vector<CommStep>& steps, const HetAnnotation& phase_src,
+               const ShardMap& in, ShardMap& out, int nthreads) {
+  if (nthreads <= 1) {
+    for (const auto& s : steps) run_step(s, phase_src, in, out);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(nthreads);
+  for (int t = 0; t < nthreads; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (const auto& s : steps) run_step(s, phase_src, in, out, t, nthreads);
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+ShardMap run_plan(const CommPlan& plan, const ShardMap& src, DType dt, int nthreads) {
   if (plan.bottom_phase.empty() && plan.top_phase.empty()) return src;
   ShardMap cur = src;
   if (!plan.bottom_phase.empty()) {
     ShardMap next = init_target(plan.bottom_target(), plan.shape, dt);
-    for (const auto& s : plan.bottom_phase) run_step(s, plan.src, cur, next);
+    run_phase(plan.bottom_phase, plan.src, cur, next, nthreads);
     cur = std::move(next);
   }
   if (!plan.top_phase.empty()) {
     ShardMap next = init_target(plan.dst, plan.shape, dt);
-    for (const auto& s : plan.top_phase) run_step(s, plan.mid ? *plan.mid : plan.src, cur, next);
+    run_phase(plan.top_phase, plan.mid ? *plan.mid : plan.src, cur, next, nthreads);
     cur = std::move(next);
   }
   return cur;
@@ -458,20 +488,28 @@ std::string cmd_execute(const std::vector<std::string>& f) {
   uint32_t seed = static_cast<uint32_t>(std::stoul(f.at(6)));
   int reps = std::stoi(f.at(8));
   int emit = std::stoi(f.at(9));
+  int nthreads = f.size() > 10 ? std::stoi(f.at(10)) : 1;
+  int warmup = f.size() > 11 ? std::stoi(f.at(11)) : 0;
   CommPlan plan = classify(src, dst, shape, dt, bw);
   ShardMap in;
   for (DeviceId d : src.all_devices())
     in.emplace(d, std::make_pair(placement(src, shape, d), make_shard(src, shape, d, seed, 0, dt)));
   ShardMap out;
-  double best = 1e30;
+  for (int r = 0; r < warmup; ++r) out = run_plan(plan, in, dt, nthreads);
+  double best = 1e30, total = 0;
   for (int r = 0; r < std::max(1, reps); ++r) {
     auto t0 = std::chrono::steady_clock::now();
-    out = run_plan(plan, in, dt);
+    out = run_plan(plan, in, dt, nthreads);
     auto t1 = std::chrono::steady_clock::now();
-    best = std::min(best, std::chrono::duration<double>(t1 - t0).count());
+    const double sec = std::chrono::duration<double>(t1 - t0).count();
+    best = std::min(best, sec);
+    total += sec;
   }
   int64_t dst_bytes = 0;
-  std::string o = "{\"seconds\":" + std::to_string(best) + ",\"shards\":{";
+  std::string o = "{\"seconds\":" + std::to_string(best) +
+                  ",\"mean\":" + std::to_string(total / std::max(1, reps)) +
+                  ",\"reps\":" + std::to_string(std::max(1, reps)) +
+                  ",\"threads\":" + std::to_string(nthreads) + ",\"shards\":{";
   bool first = true;
   for (auto& [d, rt] : out) {
     dst_bytes += rt.first.cells() * dtype_width(dt);

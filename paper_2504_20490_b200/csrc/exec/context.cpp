@@ -1,0 +1,124 @@
+// hshard-b200 executor: per-GPU context (symmetric arena, peer mapping, barriers).
+//
+// One process per GPU.  Every rank allocates an arena of the same size and
+// carves shards out of it with the same sequence of bump allocations, so an
+// (rank, offset) pair names a buffer on any GPU.  Peers' arenas are mapped
+// once through CUDA IPC (cudaIpcOpenMemHandle with lazy peer access), after
+// which a kernel on this GPU can load any peer's shard directly over NVLink.
+#include <cstring>
+#include <string>
+
+#include "program.hpp"
+
+namespace hshard::exec {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Context::Context(int rank, int world, int gpu, size_t arena_bytes)
+    : rank_(rank), world_(world), gpu_(gpu) {
+  if (world < 1 || rank < 0 || rank >= world) fail(Errc::UnknownDevice, "bad rank/world");
+  cuda_check(cudaSetDevice(gpu), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  arena_bytes_ = arena_bytes;
+  if (arena_bytes_ > 0) cuda_check(cudaMalloc(&arena_, arena_bytes_), "cudaMalloc(arena)");
+  cuda_check(cudaMalloc(&flags_, 256 * sizeof(unsigned int)), "cudaMalloc(flags)");
+  cuda_check(cudaMemset(flags_, 0, 256 * sizeof(unsigned int)), "cudaMemset(flags)");
+  cuda_check(cudaMalloc(&barrier_error_, sizeof(int)), "cudaMalloc(err)");
+  cuda_check(cudaMemset(barrier_error_, 0, sizeof(int)), "cudaMemset(err)");
+  cuda_check(cudaMalloc(&counter_, sizeof(unsigned long long)), "cudaMalloc(counter)");
+  cuda_check(cudaMalloc(&d_peer_flags_, world * sizeof(unsigned int*)), "cudaMalloc(peers)");
+  peer_arena_.assign(world, nullptr);
+  peer_flags_.assign(world, nullptr);
+  peer_arena_[rank] = arena_;
+  peer_flags_[rank] = flags_;
+  cuda_check(cudaMemcpy(d_peer_flags_, peer_flags_.data(), world * sizeof(unsigned int*),
+                        cudaMemcpyHostToDevice),
+             "cudaMemcpy(peers)");
+  cuda_check(cudaDeviceSynchronize(), "context init");
+}
+
+Context::~Context() {
+  cudaSetDevice(gpu_);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < world_; ++r) {
+    if (r == rank_) continue;
+    if (peer_arena_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
+    if (peer_flags_[r]) cudaIpcCloseMemHandle(peer_flags_[r]);
+  }
+  cudaFree(d_peer_flags_);
+  cudaFree(counter_);
+  cudaFree(barrier_error_);
+  cudaFree(flags_);
+  if (arena_) cudaFree(arena_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+char* Context::arena_of(int r) const {
+  if (r < 0 || r >= world_) fail(Errc::UnknownDevice, "rank " + std::to_string(r) + " out of range");
+  if (!peer_arena_[r]) fail(Errc::CommError, "peer arena " + std::to_string(r) + " not mapped");
+  return peer_arena_[r];
+}
+
+void Context::ipc_handles(unsigned char out[128]) const {
+  cudaIpcMemHandle_t a{}, f{};
+  if (arena_) cuda_check(cudaIpcGetMemHandle(&a, arena_), "cudaIpcGetMemHandle(arena)");
+  cuda_check(cudaIpcGetMemHandle(&f, flags_), "cudaIpcGetMemHandle(flags)");
+  std::memcpy(out, &a, 64);
+  std::memcpy(out + 64, &f, 64);
+}
+
+void Context::open_peers(const unsigned char* all) {
+  if (peers_open_) return;
+  cuda_check(cudaSetDevice(gpu_), "cudaSetDevice");
+  for (int r = 0; r < world_; ++r) {
+    if (r == rank_) continue;
+    cudaIpcMemHandle_t a, f;
+    std::memcpy(&a, all + 128 * r, 64);
+    std::memcpy(&f, all + 128 * r + 64, 64);
+    void* pa = nullptr;
+    void* pf = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle(arena)");
+    cuda_check(cudaIpcOpenMemHandle(&pf, f, cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle(flags)");
+    peer_arena_[r] = static_cast<char*>(pa);
+    peer_flags_[r] = static_cast<unsigned int*>(pf);
+  }
+  cuda_check(cudaMemcpy(d_peer_flags_, peer_flags_.data(), world_ * sizeof(unsigned int*),
+                        cudaMemcpyHostToDevice),
+             "cudaMemcpy(peers)");
+  peers_open_ = true;
+}
+
+size_t Context::alloc(size_t bytes) {
+  const size_t off = (cursor_ + 255) & ~size_t{255};
+  if (off + bytes > arena_bytes_)
+    fail(Errc::CudaError, "arena exhausted: need " + std::to_string(off + bytes) + " of " +
+                              std::to_string(arena_bytes_) + " bytes");
+  cursor_ = off + bytes;
+  return off;
+}
+
+void Context::reset_alloc(size_t offset) {
+  if (offset > arena_bytes_) fail(Errc::CudaError, "reset beyond arena");
+  cursor_ = offset;
+}
+
+void Context::barrier(cudaStream_t s) {
+  if (world_ == 1) return;
+  if (!peers_open_) fail(Errc::CommError, "barrier before open_peers");
+  ++epoch_;
+  cuda_check(launch_barrier(d_peer_flags_, world_, rank_, epoch_, 20ull * 1000 * 1000 * 1000,
+                            barrier_error_, s),
+             "barrier launch");
+}
+
+void Context::check_barrier_error() {
+  int err = 0;
+  cuda_check(cudaMemcpy(&err, barrier_error_, sizeof(int), cudaMemcpyDeviceToHost), "barrier err");
+  if (err) fail(Errc::DeadlockDetected, "cross-rank barrier timed out (a peer never arrived)");
+}
+
+}  // namespace hshard::exec

@@ -1,0 +1,575 @@
+// hshard-b200 executor: plan -> per-phase box tasks -> device tables.
+//
+// Lowering restates the executor semantics the reference specifies but never
+// implements (checked against
+// oracle/executor.py):
+//   Identity / SendRecv / Bsr / AllGather pieces -> copy tasks
+//   AllReduce / ReduceScatter -> per member: sum over the group, ascending id
+//   Split collectives -> per (slice, receiver): sum of contributors whose
+//     bottom partial ordinal p_c satisfies p_c mod P_r == p_r, ascending id;
+//     zero-fill when none does.
+// Every task is checked at compile time: a step whose members cannot produce
+// the target box (the reference's align_shard_specs defect)
+// throws Errc::UnexecutableStep instead of producing garbage.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <set>
+#include <sstream>
+
+#include "program.hpp"
+#include "hshard_c.h"
+#include <functional>
+
+namespace hshard::exec {
+
+namespace {
+
+constexpr int64_t kItemBytes = 64 * 1024;
+constexpr int kBlocksPerSm = 2;
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
+    return v;
+  }();
+  return n;
+}
+
+SliceRegion bounds_only(const SliceRegion& r) {
+  SliceRegion b;
+  b.bounds = r.bounds;
+  return b;
+}
+
+std::vector<int64_t> row_major_strides(const Shape& ext) {
+  std::vector<int64_t> s(ext.size(), 1);
+  for (int i = static_cast<int>(ext.size()) - 2; i >= 0; --i) s[i] = s[i + 1] * ext[i + 1];
+  return s;
+}
+
+}  // namespace
+
+ShardLoc& Program::loc(int state, int tensor, DeviceId d) {
+  auto it = states_[state].find({tensor, d});
+  if (it == states_[state].end())
+    fail(Errc::MissingShard, "no shard for tensor slot " + std::to_string(tensor) + " on device " +
+                                 std::to_string(d));
+  return it->second;
+}
+
+Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
+                 const std::vector<int>& v_to_rank, const size_t* src_off, const size_t* dst_off,
+                 int flags)
+    : ctx_(ctx), flags_(flags), n_virt_(static_cast<int>(v_to_rank.size())), v_to_rank_(v_to_rank) {
+  if (!comm == !sw) fail(Errc::UnsupportedOp, "program needs exactly one plan");
+  if (!ctx_.peers_open()) fail(Errc::CommError, "open peers before compiling");
+  for (int r : v_to_rank_)
+    if (r < 0 || r >= ctx_.world()) fail(Errc::UnknownDevice, "virtual device mapped to bad rank");
+  const DType dt = comm ? comm->dtype : sw->dtype;
+  dtype_ = static_cast<int>(dt);
+  es_ = dtype_width(dt);
+
+  std::vector<std::pair<const HetAnnotation*, const HetAnnotation*>> annos;
+  if (comm) {
+    shapes_.push_back(comm->shape);
+    annos.emplace_back(&comm->src, &comm->dst);
+  } else {
+    for (const SwitchEntry& e : sw->diff) {
+      shapes_.push_back(e.shape);
+      annos.emplace_back(&e.src, &e.dst);
+    }
+  }
+  n_tensors_ = static_cast<int>(shapes_.size());
+  const bool has_mid = comm && comm->mid.has_value();
+  states_.resize(has_mid ? 3 : 2);
+
+  auto add_state = [&](int state, int t, const HetAnnotation& a, const size_t* offs) {
+    for (const auto& [d, reg] : placements(a, shapes_[t])) {
+      if (d < 0 || d >= n_virt_)
+        fail(Errc::UnknownDevice, "device " + std::to_string(d) + " has no rank mapping");
+      ShardLoc L;
+      L.region = reg;
+      L.rank = v_to_rank_[d];
+      L.offset = offs ? offs[static_cast<size_t>(t) * n_virt_ + d] : SIZE_MAX;
+      states_[state][{t, d}] = L;
+    }
+  };
+  for (int t = 0; t < n_tensors_; ++t) {
+    add_state(0, t, *annos[t].first, src_off);
+    add_state(static_cast<int>(states_.size()) - 1, t, *annos[t].second, dst_off);
+  }
+  if (has_mid) {
+    // Symmetric placement of the intermediate shards: every rank packs its own
+    // mid shards densely from one common base (the max over ranks).
+    add_state(1, 0, *comm->mid, nullptr);
+    std::vector<size_t> used(ctx_.world(), 0);
+    for (auto& [key, L] : states_[1]) {
+      size_t& u = used[L.rank];
+      u = (u + 255) & ~size_t{255};
+      L.offset = u;
+      u += static_cast<size_t>(L.region.cells()) * es_;
+    }
+    const size_t base = ctx_.alloc(*std::max_element(used.begin(), used.end()) + 256);
+    for (auto& [key, L] : states_[1]) L.offset += base;
+  }
+
+  for (const auto& [key, L] : states_[0])
+    if (L.rank == ctx_.rank() && L.offset != SIZE_MAX) {
+      host_src_.emplace_back(key.second, key.first, L.offset, L.region.cells() * es_);
+      stats_.src_bytes += L.region.cells() * es_;
+    }
+  for (const auto& [key, L] : states_.back())
+    if (L.rank == ctx_.rank() && L.offset != SIZE_MAX) {
+      host_dst_.emplace_back(key.second, key.first, L.offset, L.region.cells() * es_);
+      stats_.dst_bytes += L.region.cells() * es_;
+    }
+  lower(comm, sw);
+}
+
+Program::~Program() {
+  if (dev_block_) cudaFree(dev_block_);
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
+}
+
+void Program::set_profiling(bool on) {
+  profiling_ = on;
+  events_used_ = 0;
+}
+
+int Program::phase_ms(double* out, int n) {
+  for (int p = 0; p < n; ++p) out[p] = 0;
+  const size_t per_run = 2 * static_cast<size_t>(n_phases_);
+  if (per_run == 0) return 0;
+  const int runs = static_cast<int>(events_used_ / per_run);
+  for (int r = 0; r < runs; ++r)
+    for (int p = 0; p < n_phases_ && p < n; ++p) {
+      float ms = 0;
+      cudaEvent_t a = events_[r * per_run + 2 * p], b = events_[r * per_run + 2 * p + 1];
+      cuda_check(cudaEventSynchronize(b), "event sync");
+      cuda_check(cudaEventElapsedTime(&ms, a, b), "event elapsed");
+      out[p] += ms;
+    }
+  return runs;
+}
+
+// ---------------------------------------------------------------- lowering
+namespace {
+
+struct Lowerer {
+  Program* prog;
+  std::vector<BoxTask>* out;
+  std::function<ShardLoc&(int, int, DeviceId)> loc;
+
+  BoxRef ref(int state, int t, DeviceId d, const SliceRegion& box, const char* why) {
+    const ShardLoc& L = loc(state, t, d);
+    if (!L.region.covers(box))
+      fail(Errc::UnexecutableStep, std::string(why) + ": device " + std::to_string(d) +
+                                       " holds " + L.region.str() + ", needs " + box.str());
+    BoxRef r;
+    r.rank = L.rank;
+    r.shard_offset = L.offset;
+    r.shard_ext = L.region.extents();
+    for (size_t i = 0; i < box.bounds.size(); ++i) r.lo.push_back(box.bounds[i][0] - L.region.bounds[i][0]);
+    return r;
+  }
+
+  void emit(int phase, StepKind kind, int t, int tgt, DeviceId dd, const SliceRegion& box,
+            int src, const std::vector<DeviceId>& from, const char* why) {
+    BoxTask task;
+    task.phase = phase;
+    task.kind = kind;
+    task.tensor = t;
+    task.dst_dev = dd;
+    task.dst = ref(tgt, t, dd, box, why);
+    task.box = box.extents();
+    for (DeviceId m : from) {
+      task.terms.push_back(ref(src, t, m, box, why));
+      task.term_devs.push_back(m);
+    }
+    out->push_back(std::move(task));
+  }
+};
+
+}  // namespace
+
+void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
+  std::vector<BoxTask> tasks;
+  Lowerer L{this, &tasks, [this](int s, int t, DeviceId d) -> ShardLoc& { return loc(s, t, d); }};
+  auto region_of = [this](int state, DeviceId d) { return loc(state, 0, d).region; };
+
+  auto lower_step = [&](const CommStep& step, const HetAnnotation& phase_src, int src, int tgt,
+                        int phase) {
+    switch (step.kind) {
+      case StepKind::Identity:
+        for (DeviceId d : phase_src.dg_union.at(step.subgroup).devices)
+          L.emit(phase, step.kind, 0, tgt, d, bounds_only(region_of(src, d)), src, {d}, "Identity");
+        break;
+      case StepKind::SendRecv:
+        for (const auto& [s, r] : step.pairs) {
+          const SliceRegion a = bounds_only(region_of(src, s)), b = bounds_only(region_of(tgt, r));
+          if (a.bounds != b.bounds) fail(Errc::UnexecutableStep, "SendRecv shard boxes differ");
+          L.emit(phase, step.kind, 0, tgt, r, b, src, {s}, "SendRecv");
+        }
+        break;
+      case StepKind::AllReduce:
+      case StepKind::ReduceScatter:
+        for (const auto& grp : step.groups) {
+          std::vector<DeviceId> order(grp.begin(), grp.end());
+          std::sort(order.begin(), order.end());
+          for (DeviceId d : grp)
+            L.emit(phase, step.kind, 0, tgt, d, bounds_only(region_of(tgt, d)), src, order,
+                   step_kind_name(step.kind));
+        }
+        break;
+      case StepKind::AllGather:
+        for (const auto& grp : step.groups)
+          for (DeviceId d : grp) {
+            const SliceRegion want = bounds_only(region_of(tgt, d));
+            std::vector<SliceRegion> pieces;
+            int64_t covered = 0;
+            for (DeviceId m : grp) {
+              auto isect = intersect(region_of(src, m), want);
+              if (!isect) continue;
+              for (const SliceRegion& p : pieces)
+                if (intersect(p, *isect))
+                  fail(Errc::UnexecutableStep, "AllGather members overlap on " + isect->str());
+              pieces.push_back(*isect);
+              covered += isect->cells();
+              L.emit(phase, step.kind, 0, tgt, d, *isect, src, {m}, "AllGather");
+            }
+            if (covered != want.cells())
+              fail(Errc::UnexecutableStep, "AllGather group cannot assemble " + want.str() +
+                                               " on device " + std::to_string(d));
+          }
+        break;
+      case StepKind::SplitAllReduce:
+      case StepKind::SplitReduceScatter:
+      case StepKind::SplitAllGather:
+        for (const SliceCollective& sc : step.slices) {
+          std::vector<DeviceId> cs(sc.contributors.begin(), sc.contributors.end());
+          std::sort(cs.begin(), cs.end());
+          for (DeviceId r : sc.receivers) {
+            const SliceRegion& rr = region_of(tgt, r);
+            std::vector<DeviceId> from;
+            for (DeviceId c : cs)
+              if (region_of(src, c).partial_index % rr.partial_count == rr.partial_index)
+                from.push_back(c);
+            L.emit(phase, step.kind, 0, tgt, r, sc.region, src, from, step_kind_name(step.kind));
+          }
+        }
+        break;
+      case StepKind::Bsr: {
+        const BsrPlan& b = *step.bsr;
+        for (const LocalCopy& c : b.local_copies)
+          L.emit(phase, step.kind, 0, tgt, c.device, c.region, src, {c.device}, "Bsr local");
+        for (const FusionGroup& g : b.fusion_groups)
+          for (int i : g.transfer_indices) {
+            const Transfer& t = b.transfers[i];
+            L.emit(phase, step.kind, 0, tgt, t.receiver, t.region, src, {t.sender}, "Bsr");
+          }
+        break;
+      }
+    }
+  };
+
+  if (comm) {
+    int cur = 0;
+    const HetAnnotation* cur_anno = &comm->src;
+    const int last = static_cast<int>(states_.size()) - 1;
+    int phase = 0;
+    if (!comm->bottom_phase.empty()) {
+      const int tgt = comm->mid ? 1 : last;
+      for (const CommStep& s : comm->bottom_phase) lower_step(s, *cur_anno, cur, tgt, phase);
+      cur = tgt;
+      cur_anno = comm->mid ? &*comm->mid : &comm->dst;
+      ++phase;
+    }
+    if (!comm->top_phase.empty()) {
+      for (const CommStep& s : comm->top_phase) lower_step(s, *cur_anno, cur, last, phase);
+      ++phase;
+    }
+    n_phases_ = phase;
+  } else {
+    std::map<int, int> slot;
+    for (int t = 0; t < n_tensors_; ++t) slot[sw->diff[t].tensor_id] = t;
+    auto slot_of = [&](int tid) {
+      auto it = slot.find(tid);
+      if (it == slot.end()) fail(Errc::MissingShard, "plan names unknown tensor " + std::to_string(tid));
+      return it->second;
+    };
+    for (const LocalCopy& c : sw->plan.local_copies)
+      L.emit(0, StepKind::Bsr, slot_of(c.tensor_id), 1, c.device, c.region, 0, {c.device},
+             "switch local");
+    for (const FusionGroup& g : sw->plan.fusion_groups)
+      for (int i : g.transfer_indices) {
+        const Transfer& t = sw->plan.transfers[i];
+        L.emit(0, StepKind::Bsr, slot_of(t.tensor_id), 1, t.receiver, t.region, 0, {t.sender},
+               "switch");
+      }
+    n_phases_ = 1;
+  }
+
+  // Algorithmic byte accounting over ALL ranks' tasks, then keep ours.
+  const int me = ctx_.rank();
+  std::vector<BoxTask> mine;
+  stats_.phase_bytes.assign(n_phases_, {0, 0, 0});
+  for (BoxTask& t : tasks) {
+    int64_t cells = 1;
+    for (int64_t e : t.box) cells *= e;
+    const int64_t bytes = cells * es_;
+    if (t.dst.rank == me) {
+      auto& pb = stats_.phase_bytes[t.phase];
+      stats_.hbm_write += bytes;
+      pb[1] += bytes;
+      for (const BoxRef& r : t.terms) {
+        (r.rank == me ? stats_.hbm_read : stats_.nvlink_in) += bytes;
+        pb[r.rank == me ? 0 : 2] += bytes;
+      }
+      mine.push_back(std::move(t));
+    } else {
+      for (const BoxRef& r : t.terms)
+        if (r.rank == me) stats_.nvlink_out += bytes;
+    }
+  }
+  for (const BoxTask& t : mine) {
+    if (t.dst.shard_offset == SIZE_MAX)
+      fail(Errc::MissingShard, "destination shard of device " + std::to_string(t.dst_dev) +
+                                   " has no buffer");
+    for (size_t k = 0; k < t.terms.size(); ++k)
+      if (t.terms[k].shard_offset == SIZE_MAX)
+        fail(Errc::MissingShard, "source shard of device " + std::to_string(t.term_devs[k]) +
+                                     " has no buffer");
+  }
+  if (flags_ & HS_PROG_FUSE_PHASES) fuse_phases(mine);
+  build_tables(mine);
+}
+
+void Program::fuse_phases(std::vector<BoxTask>& tasks) { (void)tasks; }
+
+// ---------------------------------------------------------------- tables
+void Program::build_tables(const std::vector<BoxTask>& tasks) {
+  struct Host {
+    std::vector<TaskDesc> tasks;
+    std::vector<TermDesc> terms;
+    std::vector<WorkItem> items[4];  // by vector width 16, 8, 4, 2
+  };
+  auto vb_slot = [](int vb) { return vb == 16 ? 0 : vb == 8 ? 1 : vb == 4 ? 2 : 3; };
+  std::vector<Host> ph(n_phases_);
+  stats_.phases = n_phases_;
+
+  for (const BoxTask& bt : tasks) {
+    Host& H = ph.at(bt.phase);
+    if (static_cast<int>(bt.terms.size()) > kMaxTerms)
+      fail(Errc::UnsupportedOp, "more than 16 terms in one reduction");
+    // refs: 0 = dst, 1.. = terms
+    std::vector<const BoxRef*> refs{&bt.dst};
+    for (const BoxRef& r : bt.terms) refs.push_back(&r);
+    const size_t nd = bt.box.size();
+    std::vector<std::vector<int64_t>> strides;
+    std::vector<int64_t> elem_off;
+    for (const BoxRef* r : refs) {
+      strides.push_back(row_major_strides(r->shard_ext));
+      int64_t off = 0;
+      for (size_t i = 0; i < nd; ++i) off += r->lo[i] * strides.back()[i];
+      elem_off.push_back(off);
+    }
+    // Drop unit dims, then merge dims that are contiguous for every ref.
+    std::vector<int64_t> ext;
+    std::vector<std::vector<int64_t>> st(refs.size());
+    for (size_t i = 0; i < nd; ++i) {
+      if (bt.box[i] == 1) continue;
+      ext.push_back(bt.box[i]);
+      for (size_t k = 0; k < refs.size(); ++k) st[k].push_back(strides[k][i]);
+    }
+    for (int i = static_cast<int>(ext.size()) - 2; i >= 0; --i) {
+      bool merge = true;
+      for (size_t k = 0; k < refs.size(); ++k)
+        merge = merge && st[k][i] == ext[i + 1] * st[k][i + 1];
+      if (!merge) continue;
+      ext[i] *= ext[i + 1];
+      ext.erase(ext.begin() + i + 1);
+      for (auto& s : st) {
+        s[i] = s[i + 1];
+        s.erase(s.begin() + i + 1);
+      }
+    }
+    if (ext.empty()) {
+      ext.push_back(1);
+      for (auto& s : st) s.push_back(1);
+    }
+    if (ext.size() > 4) fail(Errc::UnsupportedOp, "box needs more than 4 strided dims");
+    if (st[0].back() != 1 || ext.back() > INT32_MAX)
+      fail(Errc::UnsupportedOp, "innermost box dim must be contiguous and < 2^31 elements");
+    // innermost-first extents
+    const int rd = static_cast<int>(ext.size());
+    TaskDesc td{};
+    for (int j = 0; j < 4; ++j) td.n[j] = j < rd ? static_cast<int32_t>(ext[rd - 1 - j]) : 1;
+    for (int j = 1; j < 4; ++j)
+      if (j < rd && ext[rd - 1 - j] > INT32_MAX) fail(Errc::UnsupportedOp, "box dim too large");
+
+    auto addr = [&](size_t k) {
+      return ctx_.arena_of(refs[k]->rank) + refs[k]->shard_offset + elem_off[k] * es_;
+    };
+    int vb = 16;
+    auto ok = [&](int v) {
+      if (v < es_) return true;
+      if ((static_cast<int64_t>(td.n[0]) * es_) % v) return false;
+      for (size_t k = 0; k < refs.size(); ++k) {
+        if (reinterpret_cast<uintptr_t>(addr(k)) % v) return false;
+        for (int j = 1; j < rd; ++j)
+          if ((st[k][rd - 1 - j] * es_) % v) return false;
+      }
+      return true;
+    };
+    while (vb > es_ && !ok(vb)) vb /= 2;
+    if (vb < es_) vb = es_;
+    td.vec_bytes = vb;
+    td.dst = ctx_.arena_of(refs[0]->rank) + refs[0]->shard_offset + elem_off[0] * es_;
+    for (int j = 1; j < 4; ++j) td.dst_stride[j - 1] = j < rd ? st[0][rd - 1 - j] : 0;
+    td.term0 = static_cast<int32_t>(H.terms.size());
+    td.nterms = static_cast<int32_t>(bt.terms.size());
+    for (size_t k = 1; k < refs.size(); ++k) {
+      TermDesc tm{};
+      tm.base = addr(k);
+      for (int j = 1; j < 4; ++j) tm.stride[j - 1] = j < rd ? st[k][rd - 1 - j] : 0;
+      H.terms.push_back(tm);
+    }
+    const int32_t task_id = static_cast<int32_t>(H.tasks.size());
+    H.tasks.push_back(td);
+    stats_.tasks += 1;
+    stats_.terms += td.nterms;
+    (td.nterms == 0 ? stats_.zero_tasks : td.nterms == 1 ? stats_.copy_tasks : stats_.reduce_tasks) += 1;
+
+    // Work items: ~kItemBytes of output each, never crossing a (dim2, dim3) plane.
+    const int64_t row_vecs = static_cast<int64_t>(td.n[0]) * es_ / vb;
+    const int64_t target = std::max<int64_t>(1, kItemBytes / vb);
+    const int64_t planes = static_cast<int64_t>(td.n[2]) * td.n[3];
+    std::vector<WorkItem>& items = H.items[vb_slot(vb)];
+    for (int64_t pl = 0; pl < planes; ++pl) {
+      if (row_vecs >= target) {
+        for (int32_t r = 0; r < td.n[1]; ++r)
+          for (int64_t c = 0; c < row_vecs; c += target)
+            items.push_back({task_id, r, 1, static_cast<int32_t>(pl), static_cast<int32_t>(c),
+                               static_cast<int32_t>(std::min(target, row_vecs - c))});
+      } else {
+        const int32_t rows = static_cast<int32_t>(std::max<int64_t>(1, target / row_vecs));
+        for (int32_t r = 0; r < td.n[1]; r += rows)
+          items.push_back({task_id, r, std::min(rows, td.n[1] - r), static_cast<int32_t>(pl), 0,
+                             static_cast<int32_t>(row_vecs)});
+      }
+    }
+  }
+
+  // One device block for every phase's tables.
+  size_t total = 0;
+  auto reserve = [&total](size_t bytes) {
+    const size_t off = (total + 255) & ~size_t{255};
+    total = off + bytes;
+    return off;
+  };
+  struct Offs {
+    size_t tasks, terms, items[4];
+  };
+  std::vector<Offs> offs(n_phases_);
+  for (int p = 0; p < n_phases_; ++p) {
+    offs[p].tasks = reserve(ph[p].tasks.size() * sizeof(TaskDesc));
+    offs[p].terms = reserve(ph[p].terms.size() * sizeof(TermDesc));
+    for (int v = 0; v < 4; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
+  }
+  std::vector<char> host(std::max<size_t>(total, 1));
+  for (int p = 0; p < n_phases_; ++p) {
+    std::memcpy(host.data() + offs[p].tasks, ph[p].tasks.data(), ph[p].tasks.size() * sizeof(TaskDesc));
+    std::memcpy(host.data() + offs[p].terms, ph[p].terms.data(), ph[p].terms.size() * sizeof(TermDesc));
+    for (int v = 0; v < 4; ++v)
+      std::memcpy(host.data() + offs[p].items[v], ph[p].items[v].data(),
+                  ph[p].items[v].size() * sizeof(WorkItem));
+  }
+  cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
+  cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
+             "cudaMemcpy(tables)");
+  char* base = static_cast<char*>(dev_block_);
+  dphases_.resize(n_phases_);
+  const int max_grid = sm_count() * kBlocksPerSm;
+  int launches = 0;
+  for (int p = 0; p < n_phases_; ++p) {
+    DevicePhase& d = dphases_[p];
+    int64_t n = 0;
+    for (int v = 0; v < 4; ++v) {
+      const int32_t cnt = static_cast<int32_t>(ph[p].items[v].size());
+      n += cnt;
+      if (!cnt) continue;
+      Launch l;
+      l.tables = {reinterpret_cast<TaskDesc*>(base + offs[p].tasks),
+                  reinterpret_cast<TermDesc*>(base + offs[p].terms),
+                  reinterpret_cast<WorkItem*>(base + offs[p].items[v]), cnt};
+      l.vec_bytes = 16 >> v;
+      l.grid = std::max(1, std::min<int>(cnt, max_grid));
+      d.launches.push_back(l);
+      ++launches;
+    }
+    stats_.items += n;
+    stats_.phase_items.push_back(n);
+  }
+  const int barriers = ctx_.world() > 1 ? n_phases_ + 1 : 0;
+  stats_.kernels_per_run = launches + barriers;
+}
+
+// ---------------------------------------------------------------- run
+void Program::run(cudaStream_t s) {
+  if (!s) s = ctx_.stream();
+  ctx_.barrier(s);  // sources of every rank are ready
+  auto event = [&]() {
+    if (events_used_ == events_.size()) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      events_.push_back(e);
+    }
+    cuda_check(cudaEventRecord(events_[events_used_], s), "cudaEventRecord");
+    ++events_used_;
+  };
+  for (int p = 0; p < n_phases_; ++p) {
+    if (profiling_) event();
+    for (const Launch& l : dphases_[p].launches)
+      cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.grid, s), "box_phase_kernel launch");
+    if (profiling_) event();
+    ctx_.barrier(s);  // phase outputs visible to every rank / inputs released
+  }
+}
+
+void Program::run_host(const void* const* src_host, void* const* dst_host) {
+  cudaStream_t s = ctx_.stream();
+  for (const auto& [d, t, off, bytes] : host_src_) {
+    const void* h = src_host[static_cast<size_t>(t) * n_virt_ + d];
+    if (h) cuda_check(cudaMemcpyAsync(ctx_.arena() + off, h, bytes, cudaMemcpyHostToDevice, s), "H2D");
+  }
+  run(s);
+  for (const auto& [d, t, off, bytes] : host_dst_) {
+    void* h = dst_host[static_cast<size_t>(t) * n_virt_ + d];
+    if (h) cuda_check(cudaMemcpyAsync(h, ctx_.arena() + off, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+  }
+  cuda_check(cudaStreamSynchronize(s), "run_host sync");
+  ctx_.check_barrier_error();
+}
+
+std::string Program::stats_json() const {
+  std::ostringstream o;
+  o << "{\"phases\":" << stats_.phases << ",\"tasks\":" << stats_.tasks << ",\"items\":" << stats_.items
+    << ",\"terms\":" << stats_.terms << ",\"copy_tasks\":" << stats_.copy_tasks
+    << ",\"reduce_tasks\":" << stats_.reduce_tasks << ",\"zero_tasks\":" << stats_.zero_tasks
+    << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
+    << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
+    << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes
+    << ",\"kernels_per_run\":" << stats_.kernels_per_run << ",\"phase_items\":[";
+ for (size_t i = 0; i < stats_.phase_items.size(); ++i) o << (i ? "," : "") << stats_.phase_items[i];
+  o << "],\"phase_bytes\":[";
+  for (size_t i = 0; i < stats_.phase_bytes.size(); ++i)
+    o << (i ? "," : "") << "[" << stats_.phase_bytes[i][0] << "," << stats_.phase_bytes[i][1] << ","
+      << stats_.phase_bytes[i][2] << "]";
+  o << "],\"dtype\":" << dtype_ << ",\"rank\":" << ctx_.rank() << "}";
+  return o.str();
+}
+
+}  // namespace hshard::exec

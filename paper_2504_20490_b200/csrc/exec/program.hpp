@@ -1,0 +1,163 @@
+// hshard-b200 executor: host-side context and plan compiler.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hshard/resolve.hpp"
+#include "hshard/switch.hpp"
+#include "kernels.cuh"
+
+namespace hshard::exec {
+
+void cuda_check(cudaError_t e, const char* what);
+
+// Per-GPU context: one per process ("rank").  Owns the symmetric arena, the
+// barrier flag block and (after open_peers) every peer's mapped arena.
+class Context {
+ public:
+  Context(int rank, int world, int gpu, size_t arena_bytes);
+  ~Context();
+
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  int gpu() const { return gpu_; }
+  char* arena() const { return arena_; }
+  size_t arena_bytes() const { return arena_bytes_; }
+  cudaStream_t stream() const { return stream_; }
+  char* arena_of(int r) const;  // this or a peer's arena base (mapped)
+  bool peers_open() const { return world_ == 1 || peers_open_; }
+
+  void ipc_handles(unsigned char out[128]) const;
+  void open_peers(const unsigned char* all);  // world x 128 bytes, rank-major
+
+  size_t alloc(size_t bytes);  // 256-byte aligned bump allocation
+  void reset_alloc(size_t offset);
+  size_t alloc_cursor() const { return cursor_; }
+
+  // Cross-rank barrier on `s` (no-op when world == 1).
+  void barrier(cudaStream_t s);
+  void check_barrier_error();
+
+  unsigned long long* scratch_counter() const { return counter_; }
+
+ private:
+  int rank_, world_, gpu_;
+  char* arena_ = nullptr;
+  size_t arena_bytes_ = 0;
+  size_t cursor_ = 0;
+  unsigned int* flags_ = nullptr;      // world slots, written by peers
+  int* barrier_error_ = nullptr;
+  unsigned long long* counter_ = nullptr;
+  unsigned int** d_peer_flags_ = nullptr;
+  std::vector<char*> peer_arena_;
+  std::vector<unsigned int*> peer_flags_;
+  unsigned int epoch_ = 0;
+  bool peers_open_ = false;
+  cudaStream_t stream_ = nullptr;
+};
+
+// Where one tensor's shard for one virtual device lives in one layout state.
+struct ShardLoc {
+  SliceRegion region;
+  int rank = -1;
+  size_t offset = SIZE_MAX;  // arena byte offset on `rank`
+};
+
+// Host form of a box task before it is flattened into TaskDesc/TermDesc.
+struct BoxRef {
+  int rank = -1;
+  size_t shard_offset = 0;   // arena offset of the whole shard
+  Shape shard_ext;           // shard extents (row-major)
+  std::vector<int64_t> lo;   // box origin relative to the shard
+};
+
+struct BoxTask {
+  int phase = 0;
+  StepKind kind = StepKind::Identity;
+  int tensor = 0;
+  DeviceId dst_dev = -1;
+  BoxRef dst;
+  Shape box;
+  std::vector<BoxRef> terms;  // empty = zero-fill; >1 = ordered sum
+  std::vector<DeviceId> term_devs;
+};
+
+struct ProgramStats {
+  int phases = 0;
+  int64_t tasks = 0, items = 0, terms = 0;
+  int64_t copy_tasks = 0, reduce_tasks = 0, zero_tasks = 0;
+  // Algorithmic bytes per run for THIS rank:
+  int64_t hbm_read = 0;      // bytes of terms read from this GPU's HBM
+  int64_t hbm_write = 0;     // bytes written to this GPU's HBM
+  int64_t nvlink_in = 0;     // bytes of terms pulled from peers
+  int64_t nvlink_out = 0;    // bytes peers pull from this GPU
+  int64_t dst_bytes = 0;     // destination-resident bytes on this rank
+  int64_t src_bytes = 0;     // source-resident bytes on this rank
+  int kernels_per_run = 0;   // phase kernels + barrier kernels
+  std::vector<int64_t> phase_items;
+  // per phase, this rank: {local HBM read, HBM write, NVLink in (peer reads)}
+  std::vector<std::array<int64_t, 3>> phase_bytes;
+};
+
+class Program {
+ public:
+  // Plan kinds: a CommPlan (one tensor) or a fused switch plan (many tensors).
+  Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw, const std::vector<int>& v_to_rank,
+          const size_t* src_off, const size_t* dst_off, int flags);
+  ~Program();
+
+  void run(cudaStream_t s);
+  // Profiling: when enabled, run() brackets each phase's launches with CUDA
+  // events on the launching stream; phase_ms() sums the elapsed times of all
+  // runs since enabling (synchronises) and returns the run count.
+  void set_profiling(bool on);
+  int phase_ms(double* out, int n);
+  int phases() const { return n_phases_; }
+  void run_host(const void* const* src_host, void* const* dst_host);
+  const ProgramStats& stats() const { return stats_; }
+  std::string stats_json() const;
+  int dtype() const { return dtype_; }
+
+ private:
+  struct Launch {
+    PhaseTables tables{};
+    int vec_bytes = 16;
+    int grid = 1;
+  };
+  struct DevicePhase {
+    std::vector<Launch> launches;  // one per vector width present
+  };
+
+  void lower(const CommPlan* comm, const SwitchPlan* sw);
+  void build_tables(const std::vector<BoxTask>& tasks);
+  void fuse_phases(std::vector<BoxTask>& tasks);
+  ShardLoc& loc(int state, int tensor, DeviceId d);
+
+  Context& ctx_;
+  int flags_ = 0;
+  int dtype_ = 0;
+  int es_ = 4;
+  int n_virt_ = 0;
+  int n_tensors_ = 1;
+  std::vector<int> v_to_rank_;
+  std::vector<Shape> shapes_;
+  // layout states: 0 = src, 1 = mid (CommPlan with mid) / dst, 2 = dst
+  std::vector<std::map<std::pair<int, DeviceId>, ShardLoc>> states_;
+  int n_phases_ = 0;
+  std::vector<DevicePhase> dphases_;
+  void* dev_block_ = nullptr;
+  bool profiling_ = false;
+  std::vector<cudaEvent_t> events_;  // 2 per phase per profiled run
+  size_t events_used_ = 0;
+  ProgramStats stats_;
+  // host-buffer path: (virtual device, tensor) -> (offset, bytes) on this rank
+  std::vector<std::tuple<DeviceId, int, size_t, size_t>> host_src_, host_dst_;
+};
+
+}  // namespace hshard::exec

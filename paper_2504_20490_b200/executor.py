@@ -1,0 +1,266 @@
+"""Python mirror of the executor half of the C ABI (include/hshard_c.h).
+
+    ctx  = Context(arena_bytes)                          # one per process / GPU
+    lay  = ShardLayout(ctx, plan, n_virtual)             # symmetric shard buffers
+    prog = Program(ctx, plan, lay)                       # compiled tables on the GPU
+    lay.fill_src(seed)                                   # synthetic payloads (optional)
+    prog.run()                                           # device-resident reshard
+    prog.run_host(src_host, dst_host)                    # host-buffer (e2e) path
+
+This is the B200 definition of the reference's declared-but-undefined
+execute_plan (sim.hpp:77-79) / apply_switch.  Everything
+runs in libhshard_b200.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from ctypes import c_int, c_size_t, c_ulonglong, c_void_p
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import hshard as H
+from ._lib import LIB, check, i64_array, take_string
+
+SIZE_MAX = (1 << 64) - 1
+HS_PROG_FUSE_PHASES = 1
+
+NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
+              "bf16": np.uint16}
+
+
+def block_map(n_virtual: int, world: int) -> List[int]:
+    """Virtual device v -> rank v // ceil(n_virtual / world) (SURVEY §8e block mapping)."""
+    per = -(-n_virtual // world)
+    return [min(v // per, world - 1) for v in range(n_virtual)]
+
+
+class Context:
+    """hs_ctx: this process's GPU, its symmetric arena, and (world > 1) the peers' arenas."""
+
+    def __init__(self, arena_bytes: int, rank: int = 0, world: int = 1, gpu: Optional[int] = None,
+                 group=None):
+        self.rank, self.world = rank, world
+        self.gpu = rank if gpu is None else gpu
+        h = c_void_p()
+        check(LIB.hs_ctx_create(rank, world, self.gpu, arena_bytes, ctypes.byref(h)))
+        self._h = h
+        base, size = c_void_p(), c_size_t()
+        check(LIB.hs_ctx_arena(self._h, ctypes.byref(base), ctypes.byref(size)))
+        self.arena_base, self.arena_bytes = base.value, size.value
+        if world > 1:
+            self._open_peers(group)
+
+    def _open_peers(self, group):
+        import torch
+        import torch.distributed as dist
+        mine = ctypes.create_string_buffer(128)
+        check(LIB.hs_ctx_ipc_handle(self._h, mine))
+        t = torch.frombuffer(bytearray(mine.raw), dtype=torch.uint8)
+        gathered = [torch.zeros(128, dtype=torch.uint8) for _ in range(self.world)]
+        dist.all_gather(gathered, t, group=group)
+        blob = b"".join(bytes(g.numpy().tobytes()) for g in gathered)
+        check(LIB.hs_ctx_open_peers(self._h, blob))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def alloc(self, nbytes: int) -> int:
+        off = c_size_t()
+        check(LIB.hs_ctx_alloc(self._h, nbytes, ctypes.byref(off)))
+        return off.value
+
+    def reset(self, offset: int = 0) -> None:
+        check(LIB.hs_ctx_reset_alloc(self._h, offset))
+
+    def read(self, offset: int, nbytes: int) -> bytes:
+        buf = ctypes.create_string_buffer(nbytes)
+        check(LIB.hs_ctx_read(self._h, offset, buf, nbytes))
+        return buf.raw
+
+    def read_array(self, offset: int, shape, dtype: str) -> np.ndarray:
+        n = int(np.prod(shape)) if len(shape) else 1
+        out = np.empty(n, dtype=NP_STORAGE[dtype])
+        if out.nbytes:
+            check(LIB.hs_ctx_read(self._h, offset, out.ctypes.data_as(c_void_p), out.nbytes))
+        return out.reshape(shape)
+
+    def write_array(self, offset: int, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr)
+        if arr.nbytes:
+            check(LIB.hs_ctx_write(self._h, offset, arr.ctypes.data_as(c_void_p), arr.nbytes))
+
+    def sync(self) -> None:
+        check(LIB.hs_ctx_sync(self._h))
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            LIB.hs_ctx_destroy(h)
+
+    def __del__(self):
+        self.close()
+
+
+def _box(anno: str, shape, dev: int):
+    p = H.placement(anno, shape, dev)
+    return p
+
+
+class ShardLayout:
+    """Symmetric placement of every src/dst shard of a plan in the arenas.
+
+    Every rank computes the same per-rank dense packing (so it knows where each
+    peer keeps each shard), then reserves max-over-ranks bytes once; offsets
+    are identical on every rank by construction.  Keys are (tensor slot, dev).
+    """
+
+    def __init__(self, ctx: Context, plan: H.Plan, n_virtual: int,
+                 v_to_rank: Optional[Sequence[int]] = None):
+        self.ctx = ctx
+        self.plan = plan
+        self.n_virtual = n_virtual
+        self.v_to_rank = list(v_to_rank) if v_to_rank is not None else block_map(n_virtual, ctx.world)
+        self.dtype = plan.meta["dtype"]
+        self.es = H.DTYPE_BYTES[self.dtype]
+        if plan.kind == "comm":
+            self.entries = [(0, plan.meta["src"], plan.meta["dst"], list(plan.meta["shape"]))]
+        else:
+            self.entries = [(tid, s, d, list(sh)) for tid, s, d, sh in plan.meta["entries"]]
+        self.src: Dict[Tuple[int, int], dict] = {}
+        self.dst: Dict[Tuple[int, int], dict] = {}
+        self._place()
+
+    def _place(self):
+        used = [0] * self.ctx.world
+        recs = []
+        for side, store in (("src", self.src), ("dst", self.dst)):
+            for slot, (tid, s, d, shape) in enumerate(self.entries):
+                anno = s if side == "src" else d
+                devs = sorted({x for g in H.parse_annotation(anno)["groups"] for x in g})
+                for dev in devs:
+                    if dev >= self.n_virtual:
+                        raise H.HshardError("UnknownDevice", f"device {dev} >= n_virtual")
+                    p = _box(anno, shape, dev)
+                    ext = [hi - lo for lo, hi in p["bounds"]]
+                    nbytes = int(np.prod(ext)) * self.es if ext else self.es
+                    r = self.v_to_rank[dev]
+                    off = (used[r] + 255) // 256 * 256
+                    used[r] = off + nbytes
+                    rec = {"slot": slot, "dev": dev, "rank": r, "rel": off, "bytes": nbytes,
+                           "ext": ext, "bounds": p["bounds"], "partial": p["partial"],
+                           "anno": anno, "shape": shape, "tid": tid}
+                    store[(slot, dev)] = rec
+                    recs.append(rec)
+        self.base = self.ctx.alloc(max(used) + 256)
+        for rec in recs:
+            rec["offset"] = self.base + rec["rel"]
+        self.src_off = self._table(self.src)
+        self.dst_off = self._table(self.dst)
+        self.local_src_bytes = sum(r["bytes"] for r in self.src.values() if r["rank"] == self.ctx.rank)
+        self.local_dst_bytes = sum(r["bytes"] for r in self.dst.values() if r["rank"] == self.ctx.rank)
+
+    def _table(self, store):
+        n = len(self.entries) * self.n_virtual
+        arr = (c_size_t * max(1, n))(*([SIZE_MAX] * max(1, n)))
+        for (slot, dev), rec in store.items():
+            arr[slot * self.n_virtual + dev] = rec["offset"]
+        return arr
+
+    def local(self, side: str):
+        store = self.src if side == "src" else self.dst
+        return {k: v for k, v in store.items() if v["rank"] == self.ctx.rank}
+
+    # ---- payloads -------------------------------------------------------------
+    def fill_src(self, seed: int, mode: str = "grid", stream=None) -> None:
+        """Counter-hash payload into every local source shard."""
+        m = 0 if mode == "grid" else 1
+        for (slot, dev), rec in self.local("src").items():
+            arr, n = _shape_arr(rec["shape"])
+            check(LIB.hs_fill_shard(self.ctx.handle, rec["anno"].encode(), arr, n,
+                                    H.DTYPES[self.dtype], dev, rec["offset"], seed, rec["tid"], m,
+                                    stream))
+
+    def verify_dst(self, seed: int) -> int:
+        """Mismatching cells of every local dst shard vs the logical grid tensor
+        (valid for Partial-free destination annotations)."""
+        bad = 0
+        for (slot, dev), rec in self.local("dst").items():
+            arr, n = _shape_arr(rec["shape"])
+            out = c_ulonglong()
+            check(LIB.hs_verify_shard(self.ctx.handle, rec["anno"].encode(), arr, n,
+                                      H.DTYPES[self.dtype], dev, rec["offset"], seed, rec["tid"],
+                                      ctypes.byref(out), None))
+            bad += out.value
+        return bad
+
+    def read(self, side: str, slot: int, dev: int) -> np.ndarray:
+        rec = (self.src if side == "src" else self.dst)[(slot, dev)]
+        return self.ctx.read_array(rec["offset"], rec["ext"], self.dtype)
+
+    def write(self, side: str, slot: int, dev: int, arr: np.ndarray) -> None:
+        rec = (self.src if side == "src" else self.dst)[(slot, dev)]
+        assert list(arr.shape) == rec["ext"], (arr.shape, rec["ext"])
+        self.ctx.write_array(rec["offset"], arr.astype(NP_STORAGE[self.dtype], copy=False))
+
+    def clear_dst(self) -> None:
+        for rec in self.local("dst").values():
+            self.ctx.write_array(rec["offset"], np.full(rec["bytes"], 0xA5, dtype=np.uint8))
+
+
+def _shape_arr(shape):
+    return i64_array(shape), len(shape)
+
+
+class Program:
+    """hs_prog: a plan compiled for this rank."""
+
+    def __init__(self, ctx: Context, plan: H.Plan, layout: ShardLayout, flags: int = 0):
+        self.ctx, self.plan, self.layout = ctx, plan, layout
+        m = (c_int * layout.n_virtual)(*layout.v_to_rank)
+        h = c_void_p()
+        check(LIB.hs_prog_compile(ctx.handle, plan.handle, m, layout.n_virtual, layout.src_off,
+                                  layout.dst_off, flags, ctypes.byref(h)))
+        self._h = h
+
+    def run(self, stream=None) -> None:
+        check(LIB.hs_prog_run(self._h, stream))
+
+    def run_host(self, src: Dict[Tuple[int, int], np.ndarray], dst: Dict[Tuple[int, int], np.ndarray]):
+        """Host-buffer execution: src/dst keyed by (slot, dev); only this rank's shards are used."""
+        n = len(self.layout.entries) * self.layout.n_virtual
+        sp = (c_void_p * max(1, n))()
+        dp = (c_void_p * max(1, n))()
+        for (slot, dev), a in src.items():
+            sp[slot * self.layout.n_virtual + dev] = a.ctypes.data
+        for (slot, dev), a in dst.items():
+            dp[slot * self.layout.n_virtual + dev] = a.ctypes.data
+        check(LIB.hs_prog_run_host(self._h, sp, dp))
+
+    def profile(self, enable: bool = True) -> None:
+        check(LIB.hs_prog_profile(self._h, int(enable)))
+
+    def phase_ms(self):
+        """(sum of per-phase kernel ms over profiled runs, run count)."""
+        n = 8
+        out = (ctypes.c_double * n)()
+        runs = c_int()
+        check(LIB.hs_prog_phase_ms(self._h, out, n, ctypes.byref(runs)))
+        st = self.stats()
+        return [out[i] for i in range(st["phases"])], runs.value
+
+    def stats(self) -> dict:
+        out = c_void_p()
+        check(LIB.hs_prog_stats(self._h, ctypes.byref(out)))
+        return json.loads(take_string(out))
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            LIB.hs_prog_destroy(h)
+
+    def __del__(self):
+        self.close()

@@ -172,6 +172,21 @@ def config5(step: str = "S1S2") -> Workload:
 CONFIG5_CYCLE = ["S1S2", "S2S3", "S3S4", "S4S1"]
 
 
+def resident_bytes(w: Workload) -> int:
+    """Bytes of every source plus every destination shard of the workload."""
+    from .hshard import DTYPE_BYTES, parse_annotation, placement
+    total = 0
+    for tid, src, dst, shape in w.transitions:
+        for anno in (src, dst):
+            for g in parse_annotation(anno)["groups"]:
+                for d in g:
+                    n = 1
+                    for lo, hi in placement(anno, shape, d)["bounds"]:
+                        n *= hi - lo
+                    total += n * DTYPE_BYTES[w.dtype]
+    return total
+
+
 def all_workloads() -> List[Workload]:
     ws = [config1(v) for v in "ABCD"] + [config2(v) for v in "eabd"] + \
          [config3(v) for v in "bac"] + [config4()] + [config5(s) for s in CONFIG5_CYCLE]

@@ -29,7 +29,10 @@ def gpu_ctx():
     """One executor context on cuda:0 for the whole GPU test session."""
     if not cuda_available():
         pytest.skip("no GPU")
+    import torch
     from paper_2504_20490_b200 import executor
-    ctx = executor.Context(arena_bytes=int(os.environ.get("HS_TEST_ARENA_GB", "40")) << 30)
+    free, total = torch.cuda.mem_get_info(0)
+    gb = int(os.environ.get("HS_TEST_ARENA_GB", "0")) or max(4, int(free / 2**30) - 12)
+    ctx = executor.Context(arena_bytes=gb << 30)
     yield ctx
     ctx.close()
