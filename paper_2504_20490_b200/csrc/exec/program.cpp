@@ -380,7 +380,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     std::vector<int64_t> ext;
     std::vector<std::vector<int64_t>> st(refs.size());
     for (size_t i = 0; i < nd; ++i) {
-      if (bt.box[i] == 1) continue;
+      if (bt.box[i] == 1 && i + 1 < nd) continue;  // the innermost (stride-1) dim always stays
       ext.push_back(bt.box[i]);
       for (size_t k = 0; k < refs.size(); ++k) st[k].push_back(strides[k][i]);
     }
