@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--no-switch", action="store_true", help="skip the cfg4 graph-switch probe")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--fuse", action="store_true", help="compile with HS_PROG_FUSE_PHASES")
+    ap.add_argument("--flags", type=int, default=0,
+                    help="HS_PROG_* bits: 1 fuse, 2 no-fuse, 4 no-TMA, 8 no-merge (14 = plain baseline)")
     return ap.parse_args()
 
 
@@ -251,7 +252,7 @@ def main():
     import numpy as np
     import torch
     from paper_2504_20490_b200 import hshard as H
-    from paper_2504_20490_b200.executor import HS_PROG_FUSE_PHASES, Context, Program, ShardLayout
+    from paper_2504_20490_b200.executor import Context, Program, ShardLayout
 
     torch.cuda.set_device(local)
     free, _ = torch.cuda.mem_get_info(local)
@@ -278,7 +279,7 @@ def main():
         else:
             plan = H.plan_switch(work.transitions, work.dtype)
         lay = ShardLayout(ctx, plan, work.n_virtual)
-        prog = Program(ctx, plan, lay, HS_PROG_FUSE_PHASES if args.fuse else 0)
+        prog = Program(ctx, plan, lay, args.flags)
         return plan, lay, prog
 
     stream = torch.cuda.Stream(device=local)
@@ -338,7 +339,9 @@ def main():
         achieved = (rd + wr) / kern_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(w.name, dom),
-                "kernel": f"box_phase_kernel phase {dom} ({['bottom', 'top'][dom] if st['phases'] == 2 else 'plan'})",
+                "kernel": (f"{'box_phase_tma_kernel' if st['tma_items'] else 'box_phase_kernel'} "
+                           f"phase {dom} of {st['phases']} (plan phases {st['plan_phases']}, "
+                           f"fused tasks {st['fused_tasks']})"),
                 "bytes_per_launch": rd + wr, "launch_ms": phase_ms[dom],
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "share_of_step": phase_ms[dom] / ms if ms else None}
@@ -416,7 +419,10 @@ def main():
                        "plan": [s["kind"] for s in plan.json()["bottom"] + plan.json()["top"]]
                        if w.kind == "classify" else "fused Bsr",
                        "dst_resident_bytes": total_dst, "l2": "inputs larger than L2 (no flush)",
-                       "fuse_phases": bool(args.fuse)},
+                       "program_flags": args.flags,
+                       "program": {k: st[k] for k in ("phases", "plan_phases", "tasks", "items",
+                                                      "fused_tasks", "tma_items", "hbm_read",
+                                                      "hbm_write", "nvlink_in", "nvlink_out")}},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": args.steps * st["kernels_per_run"],
             "kernels_per_step": st["kernels_per_run"], "phase_ms": phase_ms,

@@ -104,7 +104,12 @@ int hs_ctx_reset_alloc(hs_ctx* ctx, size_t offset);
  * offset of that device's shard on its rank (row-major over its placement
  * box; SIZE_MAX = not present).  Intermediate (mid) shards are allocated
  * from the arena by the compiler (symmetrically). flags: HS_PROG_* bits. */
-enum { HS_PROG_FUSE_PHASES = 1, HS_PROG_NO_GRAPH = 2 };
+enum {
+  HS_PROG_FUSE_PHASES = 1, /* fuse phase-1 sums into phase-2 tasks (default when world == 1) */
+  HS_PROG_NO_FUSE = 2,     /* never fuse (materialise the mid annotation) */
+  HS_PROG_NO_TMA = 4,      /* register path only (A/B measurements) */
+  HS_PROG_NO_MERGE = 8     /* one task per destination shard (no multi-output tasks) */
+};
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);
 void hs_prog_destroy(hs_prog* prog);

@@ -20,6 +20,7 @@ Context::Context(int rank, int world, int gpu, size_t arena_bytes)
     : rank_(rank), world_(world), gpu_(gpu) {
   if (world < 1 || rank < 0 || rank >= world) fail(Errc::UnknownDevice, "bad rank/world");
   cuda_check(cudaSetDevice(gpu), "cudaSetDevice");
+  cuda_check(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, gpu), "SM count");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   arena_bytes_ = arena_bytes;
   if (arena_bytes_ > 0) cuda_check(cudaMalloc(&arena_, arena_bytes_), "cudaMalloc(arena)");

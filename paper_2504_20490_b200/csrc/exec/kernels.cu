@@ -1,15 +1,18 @@
 // hshard-b200 executor kernels (sm_100a).
 //
-// box_phase_kernel: one persistent launch per plan phase.  Each CTA walks
-// work items (grid-stride); an item is a run of rows of one task's box.
-// Per 16-byte vector a thread issues one streaming load per term (local HBM
-// or a peer GPU's HBM over NVLink), accumulates in the dtype's accumulator in
-// term order, rounds once and issues one streaming store.  Loads of UNROLL
-// vectors are in flight per thread per term, so a 2048-thread SM keeps
-// ~128 KB of reads outstanding -- enough to saturate HBM3e (and NVLink for
-// peer terms) without TMA: the boxes are already row-contiguous, there is no
-// transpose to stage through shared memory, and every byte is touched once.
+// box_phase_tma_kernel (16-byte-aligned items, the hot path):
+//   one persistent CTA per SM, warp-specialised.  Lane 0 of warp 0 is the
+//   producer: for each work item it arms a stage's mbarrier with the item's
+//   byte count and issues one cp.async.bulk (TMA bulk copy, global ->
+//   shared) per (term, row) segment.  Warps 1..15 consume: wait for the stage,
+//   read every term from shared memory, form the grouped ordered sum in the
+//   dtype's accumulator, and store the result (st.global.cs) to every output.
+//   Four 48 KB stages keep up to ~144 KB per SM in flight independently of
+//   register pressure, which is what an HBM3e stream needs.
+// box_phase_kernel (any vector width): the register path, used for boxes
+//   whose pointers / strides / row lengths are not 16-byte aligned.
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -17,9 +20,9 @@ namespace hshard::exec {
 
 namespace {
 
-constexpr int kBlock = 512;
-constexpr int kUnroll = 4;        // vectors in flight per thread (copy)
-constexpr int kUnrollReduce = 2;  // per term (reduce: accumulators live in registers)
+constexpr int kBlock = 512;     // register path
+constexpr int kTmaThreads = 512;
+constexpr int kConsumerWarps = kTmaThreads / 32 - 1;
 
 // ---------------------------------------------------------------- arithmetic
 template <class T>
@@ -79,8 +82,6 @@ template <>
 struct Raw<4> { using type = uint32_t; };
 template <>
 struct Raw<2> { using type = uint16_t; };
-template <>
-struct Raw<1> { using type = uint8_t; };
 
 template <int VB>
 __device__ __forceinline__ typename Raw<VB>::type ld_stream(const char* p) {
@@ -115,151 +116,233 @@ union Lanes {
   T e[VB / sizeof(T)];
 };
 
-struct ItemCtx {
-  char* dst_row0;       // first vector of the item in dst
-  int64_t dst_row_step; // bytes between rows
-  int32_t nvcol;
-  int32_t nvec;
-  int32_t nterms;
-};
-
-// Shared per-item term bases (computed once per item by the first threads).
-struct SharedTerms {
-  const char* row0[kMaxTerms];
-  int64_t row_step[kMaxTerms];
-};
-
-template <class T, int VB>
-__device__ __noinline__ void run_copy(const ItemCtx c, const char* src_row0, int64_t src_step) {
-  using R = typename Raw<VB>::type;
-  for (int base = threadIdx.x; base < c.nvec; base += kBlock * kUnroll) {
-    R v[kUnroll];
-    char* d[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int idx = base + u * kBlock;
-      d[u] = nullptr;
-      if (idx < c.nvec) {
-        const int r = idx / c.nvcol;
-        const int col = idx - r * c.nvcol;
-        v[u] = ld_stream<VB>(src_row0 + r * src_step + static_cast<int64_t>(col) * VB);
-        d[u] = c.dst_row0 + r * c.dst_row_step + static_cast<int64_t>(col) * VB;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (d[u]) st_stream<VB>(d[u], v[u]);
-  }
-}
-
-template <int VB>
-__device__ __noinline__ void run_zero(const ItemCtx c) {
-  using R = typename Raw<VB>::type;
-  R z;
-  memset(&z, 0, sizeof(R));
-  for (int idx = threadIdx.x; idx < c.nvec; idx += kBlock) {
-    const int r = idx / c.nvcol;
-    const int col = idx - r * c.nvcol;
-    st_stream<VB>(c.dst_row0 + r * c.dst_row_step + static_cast<int64_t>(col) * VB, z);
-  }
-}
-
-template <class T, int VB>
-__device__ __noinline__ void run_reduce(const ItemCtx c, const SharedTerms& st) {
+// Grouped ordered sum of `nterms` vectors fetched by `get(k)`:
+//   round(sum_g round_g(sum_{k in g} widen(term_k)))   (round_g only if |g| > 1)
+template <class T, int VB, class Get>
+__device__ __forceinline__ typename Raw<VB>::type grouped_sum(int nterms, int ngroups,
+                                                              const uint8_t* gsize, Get get) {
   using Ar = Arith<T>;
   using A = typename Ar::A;
   constexpr int E = VB / sizeof(T);
-  constexpr int kUnroll = kUnrollReduce;
-  for (int base = threadIdx.x; base < c.nvec; base += kBlock * kUnroll) {
-    A acc[kUnroll][E];
-    int r[kUnroll], col[kUnroll];
+  A outer[E];
+  int k = 0;
+  const int ng = ngroups ? ngroups : nterms;
+  for (int g = 0; g < ng; ++g) {
+    const int sz = ngroups ? gsize[g] : 1;
+    Lanes<T, VB> x;
+    x.raw = get(k++);
+    A inner[E];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int idx = base + u * kBlock;
-      r[u] = idx / c.nvcol;
-      col[u] = idx - r[u] * c.nvcol;
+    for (int e = 0; e < E; ++e) inner[e] = Ar::widen(x.e[e]);
+    for (int j = 1; j < sz; ++j) {
+      x.raw = get(k++);
+#pragma unroll
+      for (int e = 0; e < E; ++e) inner[e] = Ar::add(inner[e], Ar::widen(x.e[e]));
     }
-    // term 0 initialises the accumulator (no +0.0, keeps -0.0 exact)
+    if (sz > 1) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (base + u * kBlock < c.nvec) {
-        Lanes<T, VB> x;
-        x.raw = ld_stream<VB>(st.row0[0] + r[u] * st.row_step[0] + static_cast<int64_t>(col[u]) * VB);
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc[u][e] = Ar::widen(x.e[e]);
-      }
+      for (int e = 0; e < E; ++e) inner[e] = Ar::widen(Ar::narrow(inner[e]));
     }
-    for (int k = 1; k < c.nterms; ++k) {
-      const char* b = st.row0[k];
-      const int64_t rs = st.row_step[k];
-      Lanes<T, VB> x[kUnroll];
+    if (g == 0) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (base + u * kBlock < c.nvec)
-          x[u].raw = ld_stream<VB>(b + r[u] * rs + static_cast<int64_t>(col[u]) * VB);
+      for (int e = 0; e < E; ++e) outer[e] = inner[e];
+    } else {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (base + u * kBlock < c.nvec) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) acc[u][e] = Ar::add(acc[u][e], Ar::widen(x[u].e[e]));
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (base + u * kBlock < c.nvec) {
-        Lanes<T, VB> y;
-#pragma unroll
-        for (int e = 0; e < E; ++e) y.e[e] = Ar::narrow(acc[u][e]);
-        st_stream<VB>(c.dst_row0 + r[u] * c.dst_row_step + static_cast<int64_t>(col[u]) * VB, y.raw);
-      }
+      for (int e = 0; e < E; ++e) outer[e] = Ar::add(outer[e], inner[e]);
     }
   }
+  Lanes<T, VB> y;
+#pragma unroll
+  for (int e = 0; e < E; ++e) y.e[e] = Ar::narrow(outer[e]);
+  return y.raw;
 }
 
-template <class T, int VB>
-__device__ __forceinline__ void run_item(const TaskDesc& task, const WorkItem& w, const TermDesc* terms,
-                         SharedTerms& st) {
-  const int64_t es = sizeof(T);
+// Row-0 byte address and row step of an operand for a work item.
+struct RowPtr {
+  char* row0;
+  int64_t step;
+};
+
+__device__ __forceinline__ RowPtr row_ptr(const TermDesc& t, const WorkItem& w, const TaskDesc& task,
+                                          int64_t es, int vb) {
   const int32_t i2 = w.plane % task.n[2];
   const int32_t i3 = w.plane / task.n[2];
-  ItemCtx c;
-  c.dst_row_step = task.dst_stride[0] * es;
-  c.dst_row0 = task.dst + es * (w.row0 * task.dst_stride[0] + i2 * task.dst_stride[1] +
-                                i3 * task.dst_stride[2]) +
-               static_cast<int64_t>(w.vcol0) * VB;
-  c.nvcol = w.nvcol;
-  c.nvec = w.nrow * w.nvcol;
-  c.nterms = task.nterms;
-  if (task.nterms == 0) {
-    run_zero<VB>(c);
-    return;
-  }
-  auto term_row0 = [&](const TermDesc& t) {
-    return t.base + es * (w.row0 * t.stride[0] + i2 * t.stride[1] + i3 * t.stride[2]) +
-           static_cast<int64_t>(w.vcol0) * VB;
-  };
-  if (task.nterms == 1) {
-    const TermDesc t = terms[task.term0];
-    run_copy<T, VB>(c, term_row0(t), t.stride[0] * es);
-    return;
-  }
-  __syncthreads();  // previous item's readers are done with st
-  if (threadIdx.x < task.nterms) {
-    const TermDesc t = terms[task.term0 + threadIdx.x];
-    st.row0[threadIdx.x] = term_row0(t);
-    st.row_step[threadIdx.x] = t.stride[0] * es;
-  }
-  __syncthreads();
-  run_reduce<T, VB>(c, st);
+  RowPtr p;
+  p.row0 = const_cast<char*>(t.base) +
+           es * (w.row0 * t.stride[0] + i2 * t.stride[1] + i3 * t.stride[2]) +
+           static_cast<int64_t>(w.vcol0) * vb;
+  p.step = t.stride[0] * es;
+  return p;
 }
 
+// ---------------------------------------------------------------- register path
 template <class T, int VB>
 __global__ void __launch_bounds__(kBlock, 2) box_phase_kernel(PhaseTables t) {
-  __shared__ SharedTerms st;
+  __shared__ RowPtr ops[kMaxTerms + kMaxOuts];
+  __shared__ TaskDesc task_s;
+  using R = typename Raw<VB>::type;
   for (int it = blockIdx.x; it < t.n_items; it += gridDim.x) {
     const WorkItem w = t.items[it];
-    const TaskDesc task = t.tasks[w.task];
-    run_item<T, VB>(task, w, t.terms, st);
+    __syncthreads();  // previous item done with ops / task_s
+    if (threadIdx.x == 0) task_s = t.tasks[w.task];
+    __syncthreads();
+    const int nt = task_s.nterms, no = task_s.nout;
+    if (threadIdx.x < nt)
+      ops[threadIdx.x] = row_ptr(t.terms[task_s.term0 + threadIdx.x], w, task_s, sizeof(T), VB);
+    else if (threadIdx.x < nt + no)
+      ops[threadIdx.x] = row_ptr(t.terms[task_s.out0 + threadIdx.x - nt], w, task_s, sizeof(T), VB);
+    __syncthreads();
+    const int nvcol = w.nvcol, nvec = w.nrow * w.nvcol;
+    for (int v = threadIdx.x; v < nvec; v += kBlock) {
+      const int r = v / nvcol;
+      const int64_t cb = static_cast<int64_t>(v - r * nvcol) * VB;
+      R val;
+      if (nt == 0) {
+        memset(&val, 0, sizeof(R));
+      } else if (nt == 1) {
+        val = ld_stream<VB>(ops[0].row0 + r * ops[0].step + cb);
+      } else {
+        val = grouped_sum<T, VB>(nt, task_s.ngroups, task_s.gsize, [&](int k) {
+          return ld_stream<VB>(ops[k].row0 + r * ops[k].step + cb);
+        });
+      }
+      for (int o = 0; o < no; ++o) st_stream<VB>(ops[nt + o].row0 + r * ops[nt + o].step + cb, val);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- TMA path
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Waits for the barrier phase; traps (kernel error, never a hang) after ~10 s.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const unsigned long long t0 = global_ns();
+  while (!mbar_try_wait(bar, parity)) {
+    if (global_ns() - t0 > 10ull * 1000 * 1000 * 1000) asm volatile("trap;");
+  }
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct StageMeta {
+  RowPtr out[kMaxOuts];
+  int32_t nout, nterms, ngroups, nrow, nvcol, pad;
+  uint8_t gsize[16];
+};
+
+template <class T>
+__global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTables t) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* stage = smem;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(smem + kTmaStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kTmaStages);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane != 0) return;
+    // ---- producer
+    int iter = 0;
+    for (int it = blockIdx.x; it < t.n_items; it += gridDim.x, ++iter) {
+      const int s = iter % kTmaStages;
+      if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
+      const WorkItem w = t.items[it];
+      const TaskDesc task = t.tasks[w.task];
+      StageMeta& m = meta[s];
+      m.nout = task.nout;
+      m.nterms = task.nterms;
+      m.ngroups = task.ngroups;
+      m.nrow = w.nrow;
+      m.nvcol = w.nvcol;
+      for (int g = 0; g < 16; ++g) m.gsize[g] = task.gsize[g];
+      for (int o = 0; o < task.nout; ++o) m.out[o] = row_ptr(t.terms[task.out0 + o], w, task, sizeof(T), 16);
+      const uint32_t row_bytes = static_cast<uint32_t>(w.nvcol) * 16;
+      const uint32_t bytes = row_bytes * w.nrow * task.nterms;
+      mbar_arrive_expect_tx(&full[s], bytes);  // release: orders the meta writes
+      unsigned char* dst = stage + s * kStageBytes;
+      for (int k = 0; k < task.nterms; ++k) {
+        const RowPtr p = row_ptr(t.terms[task.term0 + k], w, task, sizeof(T), 16);
+        for (int r = 0; r < w.nrow; ++r, dst += row_bytes) bulk_g2s(dst, p.row0 + r * p.step, row_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  const int ctid = threadIdx.x - 32;
+  constexpr int nct = kTmaThreads - 32;
+  int iter = 0;
+  for (int it = blockIdx.x; it < t.n_items; it += gridDim.x, ++iter) {
+    const int s = iter % kTmaStages;
+    mbar_wait(&full[s], (iter / kTmaStages) & 1);
+    const StageMeta& m = meta[s];
+    const unsigned char* in = stage + s * kStageBytes;
+    const int nvcol = m.nvcol, nvec = m.nrow * m.nvcol, nt = m.nterms, no = m.nout;
+    for (int v = ctid; v < nvec; v += nct) {
+      const int r = v / nvcol;
+      const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
+      uint4 val;
+      if (nt == 0) {
+        val = make_uint4(0, 0, 0, 0);
+      } else if (nt == 1) {
+        val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
+      } else {
+        val = grouped_sum<T, 16>(nt, m.ngroups, m.gsize, [&](int k) {
+          return *reinterpret_cast<const uint4*>(in + (static_cast<size_t>(k) * nvec + v) * 16);
+        });
+      }
+      for (int o = 0; o < no; ++o) __stcs(reinterpret_cast<uint4*>(m.out[o].row0 + r * m.out[o].step + cb), val);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -315,29 +398,20 @@ __device__ float piece_real(const FillDesc& f, uint64_t lin) {
 }
 
 template <class T>
-__device__ T encode_int(int64_t v);
-template <>
-__device__ uint16_t encode_int<uint16_t>(int64_t v) {
-  return Arith<uint16_t>::narrow(static_cast<float>(v));
+__device__ T encode_int(int64_t v) {
+  if constexpr (std::is_same_v<T, uint16_t>) return Arith<uint16_t>::narrow(static_cast<float>(v));
+  else return static_cast<T>(v);
 }
-template <>
-__device__ float encode_int<float>(int64_t v) { return static_cast<float>(v); }
-template <>
-__device__ double encode_int<double>(int64_t v) { return static_cast<double>(v); }
-template <>
-__device__ int32_t encode_int<int32_t>(int64_t v) { return static_cast<int32_t>(v); }
-template <>
-__device__ int64_t encode_int<int64_t>(int64_t v) { return v; }
 
 template <class T>
 __device__ T encode_real(float v) {
-  if constexpr (sizeof(T) == 2) return Arith<uint16_t>::narrow(v);
+  if constexpr (std::is_same_v<T, uint16_t>) return Arith<uint16_t>::narrow(v);
   else return static_cast<T>(v);
 }
 
 template <class T>
 __device__ double decode(T v) {
-  if constexpr (sizeof(T) == 2) return static_cast<double>(Arith<uint16_t>::widen(v));
+  if constexpr (std::is_same_v<T, uint16_t>) return static_cast<double>(Arith<uint16_t>::widen(v));
   else return static_cast<double>(v);
 }
 
@@ -356,10 +430,11 @@ __device__ __forceinline__ uint64_t cell_lin(const FillDesc& f, int64_t c) {
 template <class T>
 __global__ void fill_kernel(FillDesc f, int64_t cells) {
   T* out = reinterpret_cast<T*>(f.dst);
+  constexpr bool kIntegral = std::is_integral_v<T> && !std::is_same_v<T, uint16_t>;
   for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cells;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t lin = cell_lin(f, c);
-    if (f.mode == 0 || std::is_integral_v<T> && sizeof(T) != 2)
+    if (f.mode == 0 || kIntegral)
       out[c] = encode_int<T>(piece_grid(f, lin));
     else
       out[c] = encode_real<T>(piece_real(f, lin));
@@ -389,16 +464,13 @@ __global__ void barrier_kernel(unsigned int* const* peer_flags, int world, int r
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot), "r"(epoch) : "memory");
   }
   unsigned int* mine = peer_flags[rank];
-  unsigned long long t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const unsigned long long t0 = global_ns();
   for (int p = 0; p < world; ++p) {
     while (true) {
       unsigned int v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + p) : "memory");
       if (static_cast<int>(v - epoch) >= 0) break;
-      unsigned long long now;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > timeout_ns) {
+      if (global_ns() - t0 > timeout_ns) {
         *error = 1;
         return;
       }
@@ -426,9 +498,22 @@ cudaError_t by_dtype(int dtype, dim3 grid, dim3 block, cudaStream_t s, Args... a
   return cudaGetLastError();
 }
 
+constexpr size_t kTmaSmem = kTmaStages * kStageBytes + kTmaStages * sizeof(StageMeta) +
+                            2 * kTmaStages * sizeof(uint64_t);
+
 template <class T>
 struct PhaseK {
-  static void launch(dim3 g, dim3 b, cudaStream_t s, PhaseTables t, int vb) {
+  static void launch(dim3 g, dim3 b, cudaStream_t s, PhaseTables t, int vb, bool tma) {
+    if (tma) {
+      static bool configured = [] {
+        cudaFuncSetAttribute(box_phase_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kTmaSmem));
+        return true;
+      }();
+      (void)configured;
+      box_phase_tma_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+      return;
+    }
     switch (vb) {
       case 16: box_phase_kernel<T, 16><<<g, b, 0, s>>>(t); break;
       case 8:
@@ -459,9 +544,12 @@ struct VerifyK {
 
 }  // namespace
 
-cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, int grid, cudaStream_t s) {
+int tma_grid(int sm_count) { return sm_count; }
+
+cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, int grid,
+                         cudaStream_t s) {
   if (t.n_items == 0) return cudaSuccess;
-  return by_dtype<PhaseK>(dtype, dim3(grid), dim3(kBlock), s, t, vec_bytes);
+  return by_dtype<PhaseK>(dtype, dim3(grid), dim3(kBlock), s, t, vec_bytes, tma);
 }
 
 cudaError_t launch_fill(const FillDesc& f, int dtype, cudaStream_t s) {

@@ -1,12 +1,15 @@
 // hshard-b200 executor: device-side descriptor tables and kernel entry points.
 //
 // A compiled program is, per plan phase, a flat table of box TASKS
-//   dst_box := zero | copy(term0) | term0 + term1 + ... (fixed order, one rounding)
-// each over a <=4-D strided box (innermost dim contiguous), and a table of
-// WORK ITEMS that cut tasks into ~32-64 KB pieces so one persistent launch
-// load-balances every box of every step of the phase across all 148 SMs.
-// Terms may point into peer GPUs' arenas (NVLink loads): the same kernel is
-// the intra-GPU box copy, the cross-GPU pull and the fused reduce-unpack.
+//   out_0 = out_1 = ... := zero | round(sum_g round_g(sum_{t in g} term_t))
+// each over a <=4-D strided box whose innermost dim is contiguous.  Terms are
+// summed in table order inside a group and groups in table order; a group of
+// size > 1 is rounded to the storage dtype before it joins the outer sum, so a
+// fused two-phase plan (phase-1 sums feeding phase-2 sums through the
+// intermediate "mid" annotation) rounds exactly where the unfused plan does.
+// A table of WORK ITEMS cuts tasks into pieces (a run of rows of one plane of
+// the box) so one persistent launch load-balances every box of a phase.
+// Terms may be peer-GPU addresses (NVLink loads); outputs are local.
 #pragma once
 
 #include <cstdint>
@@ -16,6 +19,7 @@
 namespace hshard::exec {
 
 inline constexpr int kMaxTerms = 16;
+inline constexpr int kMaxOuts = 8;
 
 struct TermDesc {
   const char* base;   // byte address of the box origin (may be a peer address)
@@ -23,13 +27,14 @@ struct TermDesc {
 };
 
 struct TaskDesc {
-  char* dst;              // byte address of the box origin
-  int64_t dst_stride[3];  // element strides of outer dims 1..3
-  int32_t n[4];           // extents; n[0] innermost (contiguous) in elements
-  int32_t term0;          // first term in the term table
-  int32_t nterms;         // 0 = zero-fill, 1 = copy, >1 = ordered sum
-  int32_t vec_bytes;      // 16/8/4/2/1: widest vector legal for every pointer and stride
-  int32_t pad;
+  int32_t n[4];       // extents; n[0] innermost (contiguous) in elements
+  int32_t out0;       // first output in the term table (base = write address)
+  int32_t nout;       // >= 1 outputs receive the same value
+  int32_t term0;      // first input term
+  int32_t nterms;     // 0 = zero-fill, 1 = copy, >1 = grouped ordered sum
+  int32_t ngroups;    // 0 = flat (every term its own group)
+  int32_t vec_bytes;  // widest vector legal for every pointer and stride
+  uint8_t gsize[16];  // group sizes when ngroups > 0
 };
 
 // A run of `nrow` consecutive rows of one (dim2, dim3) plane of a task,
@@ -50,10 +55,17 @@ struct PhaseTables {
   int32_t n_items;
 };
 
+// Shared-memory staging of the TMA kernel: kStages ring buffers of
+// kStageBytes; the host sizes 16-byte-vector items so that
+// nterms * nrow * nvcol * 16 <= kStageBytes.
+inline constexpr int kTmaStages = 4;
+inline constexpr int kStageBytes = 48 * 1024;
+
 // dtype codes follow hshard::DType (F32, F64, I32, I64, BF16).
-// All items of one launch share the vector width `vec_bytes` (the kernel is
-// specialised on it); a phase is split into at most one launch per width.
-cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, int grid, cudaStream_t s);
+// `tma`: items were sized for the TMA pipeline (16-byte vectors only).
+cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, int grid,
+                         cudaStream_t s);
+int tma_grid(int sm_count);
 
 // Counter-hash payload generator (mirror of oracle/datagen.py).
 struct FillDesc {

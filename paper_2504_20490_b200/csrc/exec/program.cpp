@@ -1,4 +1,4 @@
-// hshard-b200 executor: plan -> per-phase box tasks -> device tables.
+// hshard-b200 executor: plan -> box tasks -> (fusion, output merging) -> device tables.
 //
 // Lowering restates the executor semantics the reference specifies but never
 // implements (checked against
@@ -11,32 +11,32 @@
 // Every task is checked at compile time: a step whose members cannot produce
 // the target box (the reference's align_shard_specs defect)
 // throws Errc::UnexecutableStep instead of producing garbage.
+//
+// Two rewrites then cut HBM traffic without changing a single result bit:
+//   * phase fusion: a phase-2 task that reads the intermediate (mid) shards
+//     is split along the boxes of the phase-1 tasks that produced them and
+//     reads their inputs directly, as a grouped sum that rounds each
+//     phase-1 group exactly where the materialised mid would have;
+//   * output merging: tasks with identical inputs (replicas, SplitAG fan-out)
+//     become one task with several outputs, so inputs are read once.
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <set>
 #include <sstream>
 
-#include "program.hpp"
 #include "hshard_c.h"
-#include <functional>
+#include "planner_internal.hpp"
+#include "program.hpp"
 
 namespace hshard::exec {
 
 namespace {
 
-constexpr int64_t kItemBytes = 64 * 1024;
+constexpr int64_t kItemBytes = 64 * 1024;     // register path, output bytes per item
+constexpr int64_t kTmaItemBytes = 32 * 1024;  // TMA path upper bound (also <= stage / nterms)
 constexpr int kBlocksPerSm = 2;
-
-int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-    return v;
-  }();
-  return n;
-}
 
 SliceRegion bounds_only(const SliceRegion& r) {
   SliceRegion b;
@@ -49,6 +49,8 @@ std::vector<int64_t> row_major_strides(const Shape& ext) {
   for (int i = static_cast<int>(ext.size()) - 2; i >= 0; --i) s[i] = s[i + 1] * ext[i + 1];
   return s;
 }
+
+int64_t cells_of(const SliceRegion& r) { return r.cells(); }
 
 }  // namespace
 
@@ -85,6 +87,7 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
   n_tensors_ = static_cast<int>(shapes_.size());
   const bool has_mid = comm && comm->mid.has_value();
   states_.resize(has_mid ? 3 : 2);
+  mid_state_ = has_mid ? 1 : -1;
 
   auto add_state = [&](int state, int t, const HetAnnotation& a, const size_t* offs) {
     for (const auto& [d, reg] : placements(a, shapes_[t])) {
@@ -101,20 +104,7 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
     add_state(0, t, *annos[t].first, src_off);
     add_state(static_cast<int>(states_.size()) - 1, t, *annos[t].second, dst_off);
   }
-  if (has_mid) {
-    // Symmetric placement of the intermediate shards: every rank packs its own
-    // mid shards densely from one common base (the max over ranks).
-    add_state(1, 0, *comm->mid, nullptr);
-    std::vector<size_t> used(ctx_.world(), 0);
-    for (auto& [key, L] : states_[1]) {
-      size_t& u = used[L.rank];
-      u = (u + 255) & ~size_t{255};
-      L.offset = u;
-      u += static_cast<size_t>(L.region.cells()) * es_;
-    }
-    const size_t base = ctx_.alloc(*std::max_element(used.begin(), used.end()) + 256);
-    for (auto& [key, L] : states_[1]) L.offset += base;
-  }
+  if (has_mid) add_state(1, 0, *comm->mid, nullptr);
 
   for (const auto& [key, L] : states_[0])
     if (L.rank == ctx_.rank() && L.offset != SIZE_MAX) {
@@ -156,48 +146,29 @@ int Program::phase_ms(double* out, int n) {
 }
 
 // ---------------------------------------------------------------- lowering
-namespace {
-
-struct Lowerer {
-  Program* prog;
-  std::vector<BoxTask>* out;
-  std::function<ShardLoc&(int, int, DeviceId)> loc;
-
-  BoxRef ref(int state, int t, DeviceId d, const SliceRegion& box, const char* why) {
+void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
+  std::vector<BoxTask> tasks;
+  auto covered = [this](int state, int t, DeviceId d, const SliceRegion& box, const char* why) {
     const ShardLoc& L = loc(state, t, d);
     if (!L.region.covers(box))
-      fail(Errc::UnexecutableStep, std::string(why) + ": device " + std::to_string(d) +
-                                       " holds " + L.region.str() + ", needs " + box.str());
-    BoxRef r;
-    r.rank = L.rank;
-    r.shard_offset = L.offset;
-    r.shard_ext = L.region.extents();
-    for (size_t i = 0; i < box.bounds.size(); ++i) r.lo.push_back(box.bounds[i][0] - L.region.bounds[i][0]);
-    return r;
-  }
-
-  void emit(int phase, StepKind kind, int t, int tgt, DeviceId dd, const SliceRegion& box,
-            int src, const std::vector<DeviceId>& from, const char* why) {
+      fail(Errc::UnexecutableStep, std::string(why) + ": device " + std::to_string(d) + " holds " +
+                                       L.region.str() + ", needs " + box.str());
+  };
+  auto emit = [&](int phase, StepKind kind, int t, int tgt, DeviceId dd, const SliceRegion& box,
+                  int src, const std::vector<DeviceId>& from, const char* why) {
     BoxTask task;
     task.phase = phase;
     task.kind = kind;
     task.tensor = t;
-    task.dst_dev = dd;
-    task.dst = ref(tgt, t, dd, box, why);
-    task.box = box.extents();
+    task.box = bounds_only(box);
+    covered(tgt, t, dd, task.box, why);
+    task.dsts.push_back({tgt, dd});
     for (DeviceId m : from) {
-      task.terms.push_back(ref(src, t, m, box, why));
-      task.term_devs.push_back(m);
+      covered(src, t, m, task.box, why);
+      task.terms.push_back({src, m});
     }
-    out->push_back(std::move(task));
-  }
-};
-
-}  // namespace
-
-void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
-  std::vector<BoxTask> tasks;
-  Lowerer L{this, &tasks, [this](int s, int t, DeviceId d) -> ShardLoc& { return loc(s, t, d); }};
+    tasks.push_back(std::move(task));
+  };
   auto region_of = [this](int state, DeviceId d) { return loc(state, 0, d).region; };
 
   auto lower_step = [&](const CommStep& step, const HetAnnotation& phase_src, int src, int tgt,
@@ -205,13 +176,13 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     switch (step.kind) {
       case StepKind::Identity:
         for (DeviceId d : phase_src.dg_union.at(step.subgroup).devices)
-          L.emit(phase, step.kind, 0, tgt, d, bounds_only(region_of(src, d)), src, {d}, "Identity");
+          emit(phase, step.kind, 0, tgt, d, region_of(src, d), src, {d}, "Identity");
         break;
       case StepKind::SendRecv:
         for (const auto& [s, r] : step.pairs) {
           const SliceRegion a = bounds_only(region_of(src, s)), b = bounds_only(region_of(tgt, r));
           if (a.bounds != b.bounds) fail(Errc::UnexecutableStep, "SendRecv shard boxes differ");
-          L.emit(phase, step.kind, 0, tgt, r, b, src, {s}, "SendRecv");
+          emit(phase, step.kind, 0, tgt, r, b, src, {s}, "SendRecv");
         }
         break;
       case StepKind::AllReduce:
@@ -220,8 +191,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
           std::vector<DeviceId> order(grp.begin(), grp.end());
           std::sort(order.begin(), order.end());
           for (DeviceId d : grp)
-            L.emit(phase, step.kind, 0, tgt, d, bounds_only(region_of(tgt, d)), src, order,
-                   step_kind_name(step.kind));
+            emit(phase, step.kind, 0, tgt, d, region_of(tgt, d), src, order, step_kind_name(step.kind));
         }
         break;
       case StepKind::AllGather:
@@ -229,7 +199,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
           for (DeviceId d : grp) {
             const SliceRegion want = bounds_only(region_of(tgt, d));
             std::vector<SliceRegion> pieces;
-            int64_t covered = 0;
+            int64_t got = 0;
             for (DeviceId m : grp) {
               auto isect = intersect(region_of(src, m), want);
               if (!isect) continue;
@@ -237,10 +207,10 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
                 if (intersect(p, *isect))
                   fail(Errc::UnexecutableStep, "AllGather members overlap on " + isect->str());
               pieces.push_back(*isect);
-              covered += isect->cells();
-              L.emit(phase, step.kind, 0, tgt, d, *isect, src, {m}, "AllGather");
+              got += isect->cells();
+              emit(phase, step.kind, 0, tgt, d, *isect, src, {m}, "AllGather");
             }
-            if (covered != want.cells())
+            if (got != want.cells())
               fail(Errc::UnexecutableStep, "AllGather group cannot assemble " + want.str() +
                                                " on device " + std::to_string(d));
           }
@@ -257,18 +227,18 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
             for (DeviceId c : cs)
               if (region_of(src, c).partial_index % rr.partial_count == rr.partial_index)
                 from.push_back(c);
-            L.emit(phase, step.kind, 0, tgt, r, sc.region, src, from, step_kind_name(step.kind));
+            emit(phase, step.kind, 0, tgt, r, sc.region, src, from, step_kind_name(step.kind));
           }
         }
         break;
       case StepKind::Bsr: {
         const BsrPlan& b = *step.bsr;
         for (const LocalCopy& c : b.local_copies)
-          L.emit(phase, step.kind, 0, tgt, c.device, c.region, src, {c.device}, "Bsr local");
+          emit(phase, step.kind, 0, tgt, c.device, c.region, src, {c.device}, "Bsr local");
         for (const FusionGroup& g : b.fusion_groups)
           for (int i : g.transfer_indices) {
             const Transfer& t = b.transfers[i];
-            L.emit(phase, step.kind, 0, tgt, t.receiver, t.region, src, {t.sender}, "Bsr");
+            emit(phase, step.kind, 0, tgt, t.receiver, t.region, src, {t.sender}, "Bsr");
           }
         break;
       }
@@ -301,93 +271,253 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
       return it->second;
     };
     for (const LocalCopy& c : sw->plan.local_copies)
-      L.emit(0, StepKind::Bsr, slot_of(c.tensor_id), 1, c.device, c.region, 0, {c.device},
-             "switch local");
+      emit(0, StepKind::Bsr, slot_of(c.tensor_id), 1, c.device, c.region, 0, {c.device}, "switch local");
     for (const FusionGroup& g : sw->plan.fusion_groups)
       for (int i : g.transfer_indices) {
         const Transfer& t = sw->plan.transfers[i];
-        L.emit(0, StepKind::Bsr, slot_of(t.tensor_id), 1, t.receiver, t.region, 0, {t.sender},
-               "switch");
+        emit(0, StepKind::Bsr, slot_of(t.tensor_id), 1, t.receiver, t.region, 0, {t.sender}, "switch");
       }
     n_phases_ = 1;
   }
+  stats_.plan_phases = n_phases_;
 
-  // Algorithmic byte accounting over ALL ranks' tasks, then keep ours.
+  // ---- rewrites (results are bit-identical by construction; see header)
+  const bool fuse = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE) &&
+                    ((flags_ & HS_PROG_FUSE_PHASES) || ctx_.world() == 1);
+  if (fuse) tasks = fuse_phases(std::move(tasks));
+  auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
+  if (!(flags_ & HS_PROG_NO_MERGE)) tasks = merge_outputs(std::move(tasks), rank_of);
+
+  // Symmetric placement of the intermediate shards still materialised:
+  // every rank packs its own mid shards densely from one common base.
+  if (mid_state_ >= 0) {
+    std::set<DeviceId> used_mid;
+    for (const BoxTask& t : tasks) {
+      for (const Operand& o : t.dsts)
+        if (o.state == mid_state_) used_mid.insert(o.dev);
+      for (const Operand& o : t.terms)
+        if (o.state == mid_state_) used_mid.insert(o.dev);
+    }
+    if (!used_mid.empty()) {
+      std::vector<size_t> used(ctx_.world(), 0);
+      for (auto& [key, L] : states_[mid_state_]) {
+        if (!used_mid.count(key.second)) continue;
+        size_t& u = used[L.rank];
+        u = (u + 255) & ~size_t{255};
+        L.offset = u;
+        u += static_cast<size_t>(L.region.cells()) * es_;
+      }
+      const size_t base = ctx_.alloc(*std::max_element(used.begin(), used.end()) + 256);
+      for (auto& [key, L] : states_[mid_state_])
+        if (used_mid.count(key.second)) L.offset += base;
+    }
+  }
+
+  // ---- algorithmic byte accounting over ALL ranks' tasks, then keep ours
   const int me = ctx_.rank();
   std::vector<BoxTask> mine;
   stats_.phase_bytes.assign(n_phases_, {0, 0, 0});
   for (BoxTask& t : tasks) {
-    int64_t cells = 1;
-    for (int64_t e : t.box) cells *= e;
-    const int64_t bytes = cells * es_;
-    if (t.dst.rank == me) {
+    const int64_t bytes = cells_of(t.box) * es_;
+    const int owner = rank_of(t.dsts.front(), t.tensor);
+    if (owner == me) {
       auto& pb = stats_.phase_bytes[t.phase];
-      stats_.hbm_write += bytes;
-      pb[1] += bytes;
-      for (const BoxRef& r : t.terms) {
-        (r.rank == me ? stats_.hbm_read : stats_.nvlink_in) += bytes;
-        pb[r.rank == me ? 0 : 2] += bytes;
+      const int64_t w = bytes * static_cast<int64_t>(t.dsts.size());
+      stats_.hbm_write += w;
+      pb[1] += w;
+      for (const Operand& o : t.terms) {
+        const bool local = rank_of(o, t.tensor) == me;
+        (local ? stats_.hbm_read : stats_.nvlink_in) += bytes;
+        pb[local ? 0 : 2] += bytes;
       }
       mine.push_back(std::move(t));
     } else {
-      for (const BoxRef& r : t.terms)
-        if (r.rank == me) stats_.nvlink_out += bytes;
+      for (const Operand& o : t.terms)
+        if (rank_of(o, t.tensor) == me) stats_.nvlink_out += bytes;
     }
   }
   for (const BoxTask& t : mine) {
-    if (t.dst.shard_offset == SIZE_MAX)
-      fail(Errc::MissingShard, "destination shard of device " + std::to_string(t.dst_dev) +
-                                   " has no buffer");
-    for (size_t k = 0; k < t.terms.size(); ++k)
-      if (t.terms[k].shard_offset == SIZE_MAX)
-        fail(Errc::MissingShard, "source shard of device " + std::to_string(t.term_devs[k]) +
-                                     " has no buffer");
+    for (const Operand& o : t.dsts)
+      if (loc(o.state, t.tensor, o.dev).offset == SIZE_MAX)
+        fail(Errc::MissingShard, "destination shard of device " + std::to_string(o.dev) + " has no buffer");
+    for (const Operand& o : t.terms)
+      if (loc(o.state, t.tensor, o.dev).offset == SIZE_MAX)
+        fail(Errc::MissingShard, "source shard of device " + std::to_string(o.dev) + " has no buffer");
   }
-  if (flags_ & HS_PROG_FUSE_PHASES) fuse_phases(mine);
   build_tables(mine);
 }
 
-void Program::fuse_phases(std::vector<BoxTask>& tasks) { (void)tasks; }
+// ---------------------------------------------------------------- fusion
+std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks) {
+  // Producers of each mid shard (phase 0 tasks write exactly one mid operand).
+  std::map<DeviceId, std::vector<int>> producers;
+  for (int i = 0; i < static_cast<int>(tasks.size()); ++i)
+    if (tasks[i].phase == 0 && tasks[i].dsts.size() == 1 && tasks[i].dsts[0].state == mid_state_)
+      producers[tasks[i].dsts[0].dev].push_back(i);
+
+  std::vector<BoxTask> out;
+  std::vector<char> needed(tasks.size(), 0);
+  bool any_unfused = false;
+
+  for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
+    BoxTask& T = tasks[i];
+    if (T.phase != 1) continue;
+    if (T.terms.empty()) {  // zero-fill reads nothing
+      out.push_back(T);
+      continue;
+    }
+    // Producer tasks intersecting the box, per term.
+    std::vector<std::vector<int>> prod(T.terms.size());
+    bool ok = T.groups.empty() && !T.terms.empty();
+    for (size_t j = 0; ok && j < T.terms.size(); ++j) {
+      if (T.terms[j].state != mid_state_) {
+        ok = false;
+        break;
+      }
+      for (int p : producers[T.terms[j].dev])
+        if (intersect(tasks[p].box, T.box)) {
+          if (tasks[p].terms.empty() || !tasks[p].groups.empty()) ok = false;
+          prod[j].push_back(p);
+        }
+    }
+    // Grid of the box cut by every producer boundary.
+    detail::Cuts cuts(T.box.bounds.size());
+    if (ok) {
+      for (size_t d = 0; d < cuts.size(); ++d) {
+        const int64_t lo = T.box.bounds[d][0], hi = T.box.bounds[d][1];
+        std::set<int64_t> s{lo, hi};
+        for (const auto& list : prod)
+          for (int p : list)
+            for (int64_t v : tasks[p].box.bounds[d])
+              if (lo < v && v < hi) s.insert(v);
+        cuts[d].assign(s.begin(), s.end());
+      }
+    }
+    std::vector<BoxTask> cells;
+    if (ok) {
+      detail::for_each_grid_cell(cuts, [&](const SliceRegion& cell) {
+        if (!ok) return;
+        BoxTask N;
+        N.phase = 1;
+        N.kind = T.kind;
+        N.tensor = T.tensor;
+        N.box = cell;
+        N.dsts = T.dsts;
+        bool nested = false;
+        for (size_t j = 0; j < T.terms.size() && ok; ++j) {
+          const BoxTask* src = nullptr;
+          for (int p : prod[j])
+            if (tasks[p].box.covers(cell)) src = &tasks[p];
+          if (!src) {
+            ok = false;
+            break;
+          }
+          N.terms.insert(N.terms.end(), src->terms.begin(), src->terms.end());
+          N.groups.push_back(static_cast<int>(src->terms.size()));
+          nested = nested || src->terms.size() > 1;
+        }
+        if (!nested) N.groups.clear();
+        if (N.terms.size() > static_cast<size_t>(kMaxTerms) || N.groups.size() > 16) ok = false;
+        cells.push_back(std::move(N));
+      });
+    }
+    if (ok) {
+      stats_.fused_tasks += static_cast<int64_t>(cells.size());
+      for (BoxTask& c : cells) out.push_back(std::move(c));
+    } else {
+      any_unfused = true;
+      for (const auto& list : prod)
+        for (int p : list) needed[p] = 1;
+      // unfused tasks keep reading mid: every producer of their mid shards is needed
+      for (const Operand& o : T.terms)
+        if (o.state == mid_state_)
+          for (int p : producers[o.dev]) needed[p] = 1;
+      out.push_back(T);
+    }
+  }
+  std::vector<BoxTask> result;
+  for (int i = 0; i < static_cast<int>(tasks.size()); ++i)
+    if (tasks[i].phase == 0 && needed[i]) result.push_back(tasks[i]);
+  for (BoxTask& t : out) result.push_back(std::move(t));
+  if (!any_unfused) {  // phase 0 vanished: one launch, no intermediate
+    for (BoxTask& t : result) t.phase = 0;
+    n_phases_ = 1;
+  }
+  return result;
+}
+
+// ---------------------------------------------------------------- output merging
+std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks,
+                                            const std::function<int(const Operand&, int)>& rank_of) {
+  std::map<std::string, int> index;
+  std::vector<BoxTask> out;
+  for (BoxTask& t : tasks) {
+    std::ostringstream k;
+    k << t.phase << '|' << t.tensor << '|' << rank_of(t.dsts.front(), t.tensor) << '|';
+    for (const auto& b : t.box.bounds) k << b[0] << ',' << b[1] << ';';
+    k << '|';
+    for (const Operand& o : t.terms) k << o.state << ':' << o.dev << ',';
+    k << '|';
+    for (int g : t.groups) k << g << ',';
+    auto it = index.find(k.str());
+    if (it != index.end() && out[it->second].dsts.size() < static_cast<size_t>(kMaxOuts)) {
+      BoxTask& m = out[it->second];
+      m.dsts.insert(m.dsts.end(), t.dsts.begin(), t.dsts.end());
+      continue;
+    }
+    index[k.str()] = static_cast<int>(out.size());
+    out.push_back(std::move(t));
+  }
+  return out;
+}
 
 // ---------------------------------------------------------------- tables
 void Program::build_tables(const std::vector<BoxTask>& tasks) {
   struct Host {
     std::vector<TaskDesc> tasks;
     std::vector<TermDesc> terms;
-    std::vector<WorkItem> items[4];  // by vector width 16, 8, 4, 2
+    std::vector<WorkItem> items[5];  // [0] TMA, then register path by width 16, 8, 4, 2
   };
-  auto vb_slot = [](int vb) { return vb == 16 ? 0 : vb == 8 ? 1 : vb == 4 ? 2 : 3; };
+  auto slot_of = [](int vb, bool tma) { return tma ? 0 : vb == 16 ? 1 : vb == 8 ? 2 : vb == 4 ? 3 : 4; };
   std::vector<Host> ph(n_phases_);
   stats_.phases = n_phases_;
+  const int me = ctx_.rank();
 
   for (const BoxTask& bt : tasks) {
     Host& H = ph.at(bt.phase);
-    if (static_cast<int>(bt.terms.size()) > kMaxTerms)
-      fail(Errc::UnsupportedOp, "more than 16 terms in one reduction");
-    // refs: 0 = dst, 1.. = terms
-    std::vector<const BoxRef*> refs{&bt.dst};
-    for (const BoxRef& r : bt.terms) refs.push_back(&r);
-    const size_t nd = bt.box.size();
-    std::vector<std::vector<int64_t>> strides;
-    std::vector<int64_t> elem_off;
-    for (const BoxRef* r : refs) {
-      strides.push_back(row_major_strides(r->shard_ext));
-      int64_t off = 0;
-      for (size_t i = 0; i < nd; ++i) off += r->lo[i] * strides.back()[i];
-      elem_off.push_back(off);
-    }
-    // Drop unit dims, then merge dims that are contiguous for every ref.
+    if (static_cast<int>(bt.terms.size()) > kMaxTerms) fail(Errc::UnsupportedOp, "more than 16 terms in one task");
+    if (static_cast<int>(bt.dsts.size()) > kMaxOuts) fail(Errc::UnsupportedOp, "more than 8 outputs in one task");
+    // refs: outputs then terms
+    struct Ref {
+      const ShardLoc* L;
+      std::vector<int64_t> st;
+      int64_t elem_off;
+    };
+    std::vector<Ref> refs;
+    auto add_ref = [&](const Operand& o) {
+      const ShardLoc& L = loc(o.state, bt.tensor, o.dev);
+      Ref r{&L, row_major_strides(L.region.extents()), 0};
+      for (size_t i = 0; i < bt.box.bounds.size(); ++i)
+        r.elem_off += (bt.box.bounds[i][0] - L.region.bounds[i][0]) * r.st[i];
+      refs.push_back(std::move(r));
+    };
+    for (const Operand& o : bt.dsts) add_ref(o);
+    for (const Operand& o : bt.terms) add_ref(o);
+    const size_t nout = bt.dsts.size();
+    const Shape box = bt.box.extents();
+    const size_t nd = box.size();
+
+    // Drop unit outer dims, then merge dims contiguous for every ref.
     std::vector<int64_t> ext;
     std::vector<std::vector<int64_t>> st(refs.size());
     for (size_t i = 0; i < nd; ++i) {
-      if (bt.box[i] == 1 && i + 1 < nd) continue;  // the innermost (stride-1) dim always stays
-      ext.push_back(bt.box[i]);
-      for (size_t k = 0; k < refs.size(); ++k) st[k].push_back(strides[k][i]);
+      if (box[i] == 1 && i + 1 < nd) continue;  // the innermost (stride-1) dim always stays
+      ext.push_back(box[i]);
+      for (size_t k = 0; k < refs.size(); ++k) st[k].push_back(refs[k].st[i]);
     }
     for (int i = static_cast<int>(ext.size()) - 2; i >= 0; --i) {
       bool merge = true;
-      for (size_t k = 0; k < refs.size(); ++k)
-        merge = merge && st[k][i] == ext[i + 1] * st[k][i + 1];
+      for (size_t k = 0; k < refs.size(); ++k) merge = merge && st[k][i] == ext[i + 1] * st[k][i + 1];
       if (!merge) continue;
       ext[i] *= ext[i + 1];
       ext.erase(ext.begin() + i + 1);
@@ -401,21 +531,16 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       for (auto& s : st) s.push_back(1);
     }
     if (ext.size() > 4) fail(Errc::UnsupportedOp, "box needs more than 4 strided dims");
-    if (st[0].back() != 1 || ext.back() > INT32_MAX)
-      fail(Errc::UnsupportedOp, "innermost box dim must be contiguous and < 2^31 elements");
-    // innermost-first extents
     const int rd = static_cast<int>(ext.size());
+    for (int64_t e : ext)
+      if (e > INT32_MAX) fail(Errc::UnsupportedOp, "box dim >= 2^31");
     TaskDesc td{};
     for (int j = 0; j < 4; ++j) td.n[j] = j < rd ? static_cast<int32_t>(ext[rd - 1 - j]) : 1;
-    for (int j = 1; j < 4; ++j)
-      if (j < rd && ext[rd - 1 - j] > INT32_MAX) fail(Errc::UnsupportedOp, "box dim too large");
 
     auto addr = [&](size_t k) {
-      return ctx_.arena_of(refs[k]->rank) + refs[k]->shard_offset + elem_off[k] * es_;
+      return ctx_.arena_of(refs[k].L->rank) + refs[k].L->offset + refs[k].elem_off * es_;
     };
-    int vb = 16;
     auto ok = [&](int v) {
-      if (v < es_) return true;
       if ((static_cast<int64_t>(td.n[0]) * es_) % v) return false;
       for (size_t k = 0; k < refs.size(); ++k) {
         if (reinterpret_cast<uintptr_t>(addr(k)) % v) return false;
@@ -424,41 +549,51 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       }
       return true;
     };
+    int vb = 16;
     while (vb > es_ && !ok(vb)) vb /= 2;
     if (vb < es_) vb = es_;
     td.vec_bytes = vb;
-    td.dst = ctx_.arena_of(refs[0]->rank) + refs[0]->shard_offset + elem_off[0] * es_;
-    for (int j = 1; j < 4; ++j) td.dst_stride[j - 1] = j < rd ? st[0][rd - 1 - j] : 0;
-    td.term0 = static_cast<int32_t>(H.terms.size());
+    td.out0 = static_cast<int32_t>(H.terms.size());
+    td.nout = static_cast<int32_t>(nout);
+    td.term0 = td.out0 + td.nout;
     td.nterms = static_cast<int32_t>(bt.terms.size());
-    for (size_t k = 1; k < refs.size(); ++k) {
+    td.ngroups = static_cast<int32_t>(bt.groups.size());
+    for (size_t g = 0; g < bt.groups.size(); ++g) td.gsize[g] = static_cast<uint8_t>(bt.groups[g]);
+    bool all_local = true;
+    for (size_t k = 0; k < refs.size(); ++k) {
       TermDesc tm{};
       tm.base = addr(k);
       for (int j = 1; j < 4; ++j) tm.stride[j - 1] = j < rd ? st[k][rd - 1 - j] : 0;
       H.terms.push_back(tm);
+      all_local = all_local && refs[k].L->rank == me;
     }
+    const bool tma = vb == 16 && all_local && !(flags_ & HS_PROG_NO_TMA);
     const int32_t task_id = static_cast<int32_t>(H.tasks.size());
     H.tasks.push_back(td);
     stats_.tasks += 1;
     stats_.terms += td.nterms;
+    stats_.outputs += td.nout;
     (td.nterms == 0 ? stats_.zero_tasks : td.nterms == 1 ? stats_.copy_tasks : stats_.reduce_tasks) += 1;
 
-    // Work items: ~kItemBytes of output each, never crossing a (dim2, dim3) plane.
+    // Work items: never crossing a (dim2, dim3) plane; TMA items also fit a
+    // pipeline stage (nterms x item bytes <= kStageBytes).
     const int64_t row_vecs = static_cast<int64_t>(td.n[0]) * es_ / vb;
-    const int64_t target = std::max<int64_t>(1, kItemBytes / vb);
+    int64_t item_bytes = kItemBytes;
+    if (tma) item_bytes = std::min<int64_t>(kTmaItemBytes, kStageBytes / std::max(1, td.nterms));
+    const int64_t target = std::max<int64_t>(1, item_bytes / vb);
     const int64_t planes = static_cast<int64_t>(td.n[2]) * td.n[3];
-    std::vector<WorkItem>& items = H.items[vb_slot(vb)];
+    std::vector<WorkItem>& items = H.items[slot_of(vb, tma)];
     for (int64_t pl = 0; pl < planes; ++pl) {
       if (row_vecs >= target) {
         for (int32_t r = 0; r < td.n[1]; ++r)
           for (int64_t c = 0; c < row_vecs; c += target)
             items.push_back({task_id, r, 1, static_cast<int32_t>(pl), static_cast<int32_t>(c),
-                               static_cast<int32_t>(std::min(target, row_vecs - c))});
+                             static_cast<int32_t>(std::min(target, row_vecs - c))});
       } else {
         const int32_t rows = static_cast<int32_t>(std::max<int64_t>(1, target / row_vecs));
         for (int32_t r = 0; r < td.n[1]; r += rows)
           items.push_back({task_id, r, std::min(rows, td.n[1] - r), static_cast<int32_t>(pl), 0,
-                             static_cast<int32_t>(row_vecs)});
+                           static_cast<int32_t>(row_vecs)});
       }
     }
   }
@@ -471,19 +606,19 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     return off;
   };
   struct Offs {
-    size_t tasks, terms, items[4];
+    size_t tasks, terms, items[5];
   };
   std::vector<Offs> offs(n_phases_);
   for (int p = 0; p < n_phases_; ++p) {
     offs[p].tasks = reserve(ph[p].tasks.size() * sizeof(TaskDesc));
     offs[p].terms = reserve(ph[p].terms.size() * sizeof(TermDesc));
-    for (int v = 0; v < 4; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
+    for (int v = 0; v < 5; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
   }
   std::vector<char> host(std::max<size_t>(total, 1));
   for (int p = 0; p < n_phases_; ++p) {
     std::memcpy(host.data() + offs[p].tasks, ph[p].tasks.data(), ph[p].tasks.size() * sizeof(TaskDesc));
     std::memcpy(host.data() + offs[p].terms, ph[p].terms.data(), ph[p].terms.size() * sizeof(TermDesc));
-    for (int v = 0; v < 4; ++v)
+    for (int v = 0; v < 5; ++v)
       std::memcpy(host.data() + offs[p].items[v], ph[p].items[v].data(),
                   ph[p].items[v].size() * sizeof(WorkItem));
   }
@@ -491,13 +626,13 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
              "cudaMemcpy(tables)");
   char* base = static_cast<char*>(dev_block_);
-  dphases_.resize(n_phases_);
-  const int max_grid = sm_count() * kBlocksPerSm;
+  dphases_.assign(n_phases_, {});
+  const int max_grid = ctx_.sm_count() * kBlocksPerSm;
   int launches = 0;
   for (int p = 0; p < n_phases_; ++p) {
     DevicePhase& d = dphases_[p];
     int64_t n = 0;
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 5; ++v) {
       const int32_t cnt = static_cast<int32_t>(ph[p].items[v].size());
       n += cnt;
       if (!cnt) continue;
@@ -505,8 +640,11 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables = {reinterpret_cast<TaskDesc*>(base + offs[p].tasks),
                   reinterpret_cast<TermDesc*>(base + offs[p].terms),
                   reinterpret_cast<WorkItem*>(base + offs[p].items[v]), cnt};
-      l.vec_bytes = 16 >> v;
-      l.grid = std::max(1, std::min<int>(cnt, max_grid));
+      l.tma = v == 0;
+      l.vec_bytes = v <= 1 ? 16 : 16 >> (v - 1);
+      l.grid = l.tma ? std::max(1, std::min<int>(cnt, tma_grid(ctx_.sm_count())))
+                     : std::max(1, std::min<int>(cnt, max_grid));
+      if (l.tma) stats_.tma_items += cnt;
       d.launches.push_back(l);
       ++launches;
     }
@@ -520,7 +658,6 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
 // ---------------------------------------------------------------- run
 void Program::run(cudaStream_t s) {
   if (!s) s = ctx_.stream();
-  ctx_.barrier(s);  // sources of every rank are ready
   auto event = [&]() {
     if (events_used_ == events_.size()) {
       cudaEvent_t e;
@@ -530,10 +667,11 @@ void Program::run(cudaStream_t s) {
     cuda_check(cudaEventRecord(events_[events_used_], s), "cudaEventRecord");
     ++events_used_;
   };
+  ctx_.barrier(s);  // sources of every rank are ready
   for (int p = 0; p < n_phases_; ++p) {
     if (profiling_) event();
     for (const Launch& l : dphases_[p].launches)
-      cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.grid, s), "box_phase_kernel launch");
+      cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.tma, l.grid, s), "box_phase launch");
     if (profiling_) event();
     ctx_.barrier(s);  // phase outputs visible to every rank / inputs released
   }
@@ -556,14 +694,16 @@ void Program::run_host(const void* const* src_host, void* const* dst_host) {
 
 std::string Program::stats_json() const {
   std::ostringstream o;
-  o << "{\"phases\":" << stats_.phases << ",\"tasks\":" << stats_.tasks << ",\"items\":" << stats_.items
-    << ",\"terms\":" << stats_.terms << ",\"copy_tasks\":" << stats_.copy_tasks
+  o << "{\"phases\":" << stats_.phases << ",\"plan_phases\":" << stats_.plan_phases
+    << ",\"tasks\":" << stats_.tasks << ",\"items\":" << stats_.items << ",\"terms\":" << stats_.terms
+    << ",\"outputs\":" << stats_.outputs << ",\"copy_tasks\":" << stats_.copy_tasks
     << ",\"reduce_tasks\":" << stats_.reduce_tasks << ",\"zero_tasks\":" << stats_.zero_tasks
+    << ",\"tma_items\":" << stats_.tma_items << ",\"fused_tasks\":" << stats_.fused_tasks
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes
     << ",\"kernels_per_run\":" << stats_.kernels_per_run << ",\"phase_items\":[";
- for (size_t i = 0; i < stats_.phase_items.size(); ++i) o << (i ? "," : "") << stats_.phase_items[i];
+  for (size_t i = 0; i < stats_.phase_items.size(); ++i) o << (i ? "," : "") << stats_.phase_items[i];
   o << "],\"phase_bytes\":[";
   for (size_t i = 0; i < stats_.phase_bytes.size(); ++i)
     o << (i ? "," : "") << "[" << stats_.phase_bytes[i][0] << "," << stats_.phase_bytes[i][1] << ","

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -32,6 +33,7 @@ class Context {
   cudaStream_t stream() const { return stream_; }
   char* arena_of(int r) const;  // this or a peer's arena base (mapped)
   bool peers_open() const { return world_ == 1 || peers_open_; }
+  int sm_count() const { return sm_count_; }
 
   void ipc_handles(unsigned char out[128]) const;
   void open_peers(const unsigned char* all);  // world x 128 bytes, rank-major
@@ -48,10 +50,11 @@ class Context {
 
  private:
   int rank_, world_, gpu_;
+  int sm_count_ = 148;
   char* arena_ = nullptr;
   size_t arena_bytes_ = 0;
   size_t cursor_ = 0;
-  unsigned int* flags_ = nullptr;      // world slots, written by peers
+  unsigned int* flags_ = nullptr;  // world slots, written by peers
   int* barrier_error_ = nullptr;
   unsigned long long* counter_ = nullptr;
   unsigned int** d_peer_flags_ = nullptr;
@@ -69,29 +72,32 @@ struct ShardLoc {
   size_t offset = SIZE_MAX;  // arena byte offset on `rank`
 };
 
-// Host form of a box task before it is flattened into TaskDesc/TermDesc.
-struct BoxRef {
-  int rank = -1;
-  size_t shard_offset = 0;   // arena offset of the whole shard
-  Shape shard_ext;           // shard extents (row-major)
-  std::vector<int64_t> lo;   // box origin relative to the shard
+// A shard in a layout state: (state, virtual device); the tensor is the task's.
+struct Operand {
+  int state = 0;
+  DeviceId dev = -1;
+  bool operator==(const Operand&) const = default;
+  bool operator<(const Operand& o) const { return state != o.state ? state < o.state : dev < o.dev; }
 };
 
+// One box task in logical coordinates:
+//   every dst := zero | round(sum_g round_g(sum_{t in g} term_t))
 struct BoxTask {
   int phase = 0;
   StepKind kind = StepKind::Identity;
   int tensor = 0;
-  DeviceId dst_dev = -1;
-  BoxRef dst;
-  Shape box;
-  std::vector<BoxRef> terms;  // empty = zero-fill; >1 = ordered sum
-  std::vector<DeviceId> term_devs;
+  SliceRegion box;              // logical coordinates (bounds only)
+  std::vector<Operand> dsts;    // >= 1, all on one rank
+  std::vector<Operand> terms;   // summation order; empty = zero-fill
+  std::vector<int> groups;      // sizes; empty = flat (each term its own group)
 };
 
 struct ProgramStats {
-  int phases = 0;
-  int64_t tasks = 0, items = 0, terms = 0;
-  int64_t copy_tasks = 0, reduce_tasks = 0, zero_tasks = 0;
+  int phases = 0;            // launched phases after fusion
+  int plan_phases = 0;       // phases of the plan
+  int64_t tasks = 0, items = 0, terms = 0, outputs = 0;
+  int64_t copy_tasks = 0, reduce_tasks = 0, zero_tasks = 0, tma_items = 0;
+  int64_t fused_tasks = 0;   // phase-2 tasks that read phase-1 inputs directly
   // Algorithmic bytes per run for THIS rank:
   int64_t hbm_read = 0;      // bytes of terms read from this GPU's HBM
   int64_t hbm_write = 0;     // bytes written to this GPU's HBM
@@ -101,7 +107,7 @@ struct ProgramStats {
   int64_t src_bytes = 0;     // source-resident bytes on this rank
   int kernels_per_run = 0;   // phase kernels + barrier kernels
   std::vector<int64_t> phase_items;
-  // per phase, this rank: {local HBM read, HBM write, NVLink in (peer reads)}
+  // per launched phase, this rank: {local HBM read, HBM write, NVLink in}
   std::vector<std::array<int64_t, 3>> phase_bytes;
 };
 
@@ -113,13 +119,13 @@ class Program {
   ~Program();
 
   void run(cudaStream_t s);
+  void run_host(const void* const* src_host, void* const* dst_host);
   // Profiling: when enabled, run() brackets each phase's launches with CUDA
   // events on the launching stream; phase_ms() sums the elapsed times of all
   // runs since enabling (synchronises) and returns the run count.
   void set_profiling(bool on);
   int phase_ms(double* out, int n);
   int phases() const { return n_phases_; }
-  void run_host(const void* const* src_host, void* const* dst_host);
   const ProgramStats& stats() const { return stats_; }
   std::string stats_json() const;
   int dtype() const { return dtype_; }
@@ -128,15 +134,18 @@ class Program {
   struct Launch {
     PhaseTables tables{};
     int vec_bytes = 16;
+    bool tma = false;
     int grid = 1;
   };
   struct DevicePhase {
-    std::vector<Launch> launches;  // one per vector width present
+    std::vector<Launch> launches;  // TMA launch + one per vector width present
   };
 
   void lower(const CommPlan* comm, const SwitchPlan* sw);
+  std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks);
+  static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks,
+                                            const std::function<int(const Operand&, int)>& rank_of);
   void build_tables(const std::vector<BoxTask>& tasks);
-  void fuse_phases(std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);
 
   Context& ctx_;
@@ -145,6 +154,7 @@ class Program {
   int es_ = 4;
   int n_virt_ = 0;
   int n_tensors_ = 1;
+  int mid_state_ = -1;  // layout state index of the plan's mid annotation
   std::vector<int> v_to_rank_;
   std::vector<Shape> shapes_;
   // layout states: 0 = src, 1 = mid (CommPlan with mid) / dst, 2 = dst

@@ -25,7 +25,11 @@ from . import hshard as H
 from ._lib import LIB, check, i64_array, take_string
 
 SIZE_MAX = (1 << 64) - 1
-HS_PROG_FUSE_PHASES = 1
+HS_PROG_FUSE_PHASES = 1   # fuse phase-1 sums into phase-2 tasks (default when world == 1)
+HS_PROG_NO_FUSE = 2       # materialise the mid annotation
+HS_PROG_NO_TMA = 4        # register path only
+HS_PROG_NO_MERGE = 8      # one task per destination shard
+HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
               "bf16": np.uint16}

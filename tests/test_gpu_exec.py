@@ -26,25 +26,33 @@ from paper_2504_20490_b200 import workloads as W
 pytestmark = pytest.mark.gpu
 
 
-def _gpu_case(ctx, plan, src, dst, shape, dtype, seed, mode, n_virtual=10):
+FLAG_SETS = [0, 2 | 4 | 8]  # default (fused, TMA, merged outputs) and the plain register path
+
+
+def _gpu_case(ctx, plan, src, dst, shape, dtype, seed, mode, n_virtual=10, flag_sets=FLAG_SETS):
     from paper_2504_20490_b200.executor import Program, ShardLayout
     mark = ctx.alloc(0)
     try:
         lay = ShardLayout(ctx, plan, n_virtual)
         lay.fill_src(seed, mode)
-        lay.clear_dst()
         ref_src = ox.scatter(src, shape, dtype, seed, 0, mode)
         for (slot, dev) in lay.src:
             got = lay.read("src", 0, dev)
             assert np.array_equal(got.view(np.uint8), ref_src[dev].view(np.uint8)), ("fill", dev)
-        prog = Program(ctx, plan, lay)
-        prog.run()
-        ctx.sync()
         want = ox.execute_plan(plan.json(), ref_src, dtype)
-        for (slot, dev) in lay.dst:
-            got = lay.read("dst", 0, dev)
-            assert np.array_equal(got.view(np.uint8), want[dev].view(np.uint8)), (src, dst, dev)
-        return prog.stats()
+        stats = None
+        for flags in flag_sets:
+            lay.clear_dst()
+            prog = Program(ctx, plan, lay, flags)
+            prog.run()
+            ctx.sync()
+            for (slot, dev) in lay.dst:
+                got = lay.read("dst", 0, dev)
+                assert np.array_equal(got.view(np.uint8), want[dev].view(np.uint8)), \
+                    (flags, src, dst, dev)
+            stats = stats or prog.stats()
+            prog.close()
+        return stats
     finally:
         ctx.reset(mark)
 
