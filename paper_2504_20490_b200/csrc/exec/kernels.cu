@@ -21,8 +21,8 @@ namespace hshard::exec {
 namespace {
 
 constexpr int kBlock = 512;     // register path
-constexpr int kTmaThreads = 512;
-constexpr int kConsumerWarps = kTmaThreads / 32 - 1;
+constexpr int kConsumerWarps = 16;                   // 512 consumer threads
+constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
 
 // ---------------------------------------------------------------- arithmetic
 template <class T>
@@ -176,8 +176,8 @@ __device__ __forceinline__ RowPtr row_ptr(const TermDesc& t, const WorkItem& w, 
 }
 
 // ---------------------------------------------------------------- register path
-template <class T, int VB>
-__global__ void __launch_bounds__(kBlock, 2) box_phase_kernel(PhaseTables t) {
+template <class T, int VB, bool kReduce>
+__global__ void __launch_bounds__(kBlock, kReduce ? 1 : 2) box_phase_kernel(PhaseTables t) {
   __shared__ RowPtr ops[kMaxTerms + kMaxOuts];
   __shared__ TaskDesc task_s;
   using R = typename Raw<VB>::type;
@@ -193,20 +193,79 @@ __global__ void __launch_bounds__(kBlock, 2) box_phase_kernel(PhaseTables t) {
       ops[threadIdx.x] = row_ptr(t.terms[task_s.out0 + threadIdx.x - nt], w, task_s, sizeof(T), VB);
     __syncthreads();
     const int nvcol = w.nvcol, nvec = w.nrow * w.nvcol;
-    for (int v = threadIdx.x; v < nvec; v += kBlock) {
-      const int r = v / nvcol;
-      const int64_t cb = static_cast<int64_t>(v - r * nvcol) * VB;
-      R val;
-      if (nt == 0) {
-        memset(&val, 0, sizeof(R));
-      } else if (nt == 1) {
-        val = ld_stream<VB>(ops[0].row0 + r * ops[0].step + cb);
-      } else {
-        val = grouped_sum<T, VB>(nt, task_s.ngroups, task_s.gsize, [&](int k) {
-          return ld_stream<VB>(ops[k].row0 + r * ops[k].step + cb);
-        });
+    if constexpr (!kReduce) {
+      // copy / zero: kCopyUnroll independent 16-byte loads in flight per thread
+      constexpr int U = 4;
+      for (int base = threadIdx.x; base < nvec; base += kBlock * U) {
+        R val[U];
+        int r[U];
+        int64_t cb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int v = base + u * kBlock;
+          r[u] = v / nvcol;
+          cb[u] = static_cast<int64_t>(v - r[u] * nvcol) * VB;
+          if (nt == 0)
+            memset(&val[u], 0, sizeof(R));
+          else if (v < nvec)
+            val[u] = ld_stream<VB>(ops[0].row0 + r[u] * ops[0].step + cb[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (base + u * kBlock < nvec)
+            for (int o = 0; o < no; ++o)
+              st_stream<VB>(ops[nt + o].row0 + r[u] * ops[nt + o].step + cb[u], val[u]);
       }
-      for (int o = 0; o < no; ++o) st_stream<VB>(ops[nt + o].row0 + r * ops[nt + o].step + cb, val);
+    } else {
+    // grouped ordered sum, U vectors in lock-step so U loads per term are in flight
+    using Ar = Arith<T>;
+    using A = typename Ar::A;
+    constexpr int E = VB / sizeof(T);
+    constexpr int U = 2;
+    const int ng = task_s.ngroups ? task_s.ngroups : nt;
+    for (int base = threadIdx.x; base < nvec; base += kBlock * U) {
+      int r[U];
+      int64_t cb[U];
+      bool on[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = base + u * kBlock;
+        on[u] = v < nvec;
+        r[u] = v / nvcol;
+        cb[u] = static_cast<int64_t>(v - r[u] * nvcol) * VB;
+      }
+      A outer[U][E], inner[U][E];
+      int k = 0;
+      for (int g = 0; g < ng; ++g) {
+        const int sz = task_s.ngroups ? task_s.gsize[g] : 1;
+        for (int j = 0; j < sz; ++j, ++k) {
+          Lanes<T, VB> x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (on[u]) x[u].raw = ld_stream<VB>(ops[k].row0 + r[u] * ops[k].step + cb[u]);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              inner[u][e] = j == 0 ? Ar::widen(x[u].e[e]) : Ar::add(inner[u][e], Ar::widen(x[u].e[e]));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const A v = sz > 1 ? Ar::widen(Ar::narrow(inner[u][e])) : inner[u][e];
+            outer[u][e] = g == 0 ? v : Ar::add(outer[u][e], v);
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!on[u]) continue;
+        Lanes<T, VB> y;
+#pragma unroll
+        for (int e = 0; e < E; ++e) y.e[e] = Ar::narrow(outer[u][e]);
+        for (int o = 0; o < no; ++o) st_stream<VB>(ops[nt + o].row0 + r[u] * ops[nt + o].step + cb[u], y.raw);
+      }
+    }
     }
   }
 }
@@ -264,18 +323,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-struct StageMeta {
-  RowPtr out[kMaxOuts];
-  int32_t nout, nterms, ngroups, nrow, nvcol, pad;
-  uint8_t gsize[16];
-};
-
 template <class T>
 __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTables t) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* stage = smem;
-  StageMeta* meta = reinterpret_cast<StageMeta*>(smem + kTmaStages * kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kTmaStages);
+  uint4* meta = reinterpret_cast<uint4*>(smem + kTmaStages * kStageBytes);  // 32 words per stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kTmaStages * 32);
   uint64_t* empty = full + kTmaStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -286,31 +339,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const int W = t.rec_words;
 
   if (warp == 0) {
-    if (lane != 0) return;
-    // ---- producer
+    // ---- producer warp: the item record is prefetched one item ahead (one
+    // 16-byte word per lane); lane k then streams term k's rows.
     int iter = 0;
-    for (int it = blockIdx.x; it < t.n_items; it += gridDim.x, ++iter) {
+    int it = blockIdx.x;
+    uint4 next = make_uint4(0, 0, 0, 0);
+    if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+    for (; it < t.n_items; it += gridDim.x, ++iter) {
+      const uint4 cur = next;
+      const int nit = it + gridDim.x;
+      if (nit < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nit) * W + lane];
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
-      const WorkItem w = t.items[it];
-      const TaskDesc task = t.tasks[w.task];
-      StageMeta& m = meta[s];
-      m.nout = task.nout;
-      m.nterms = task.nterms;
-      m.ngroups = task.ngroups;
-      m.nrow = w.nrow;
-      m.nvcol = w.nvcol;
-      for (int g = 0; g < 16; ++g) m.gsize[g] = task.gsize[g];
-      for (int o = 0; o < task.nout; ++o) m.out[o] = row_ptr(t.terms[task.out0 + o], w, task, sizeof(T), 16);
-      const uint32_t row_bytes = static_cast<uint32_t>(w.nvcol) * 16;
-      const uint32_t bytes = row_bytes * w.nrow * task.nterms;
-      mbar_arrive_expect_tx(&full[s], bytes);  // release: orders the meta writes
-      unsigned char* dst = stage + s * kStageBytes;
-      for (int k = 0; k < task.nterms; ++k) {
-        const RowPtr p = row_ptr(t.terms[task.term0 + k], w, task, sizeof(T), 16);
-        for (int r = 0; r < w.nrow; ++r, dst += row_bytes) bulk_g2s(dst, p.row0 + r * p.step, row_bytes, &full[s]);
+      uint4* m = meta + s * 32;
+      if (lane < W) m[lane] = cur;
+      __syncwarp();
+      const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
+      const int nt = h->nterms, nrow = h->nrow;
+      const uint32_t row_bytes = static_cast<uint32_t>(h->nvcol) * 16;
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], row_bytes * nrow * nt);  // release: meta
+      __syncwarp();
+      if (lane < nt) {
+        const TmaOperand op = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords)[lane];
+        unsigned char* dst = stage + s * kStageBytes + static_cast<size_t>(lane) * nrow * row_bytes;
+        for (int r = 0; r < nrow; ++r) bulk_g2s(dst + r * row_bytes, op.row0 + r * op.step, row_bytes, &full[s]);
       }
     }
     return;
@@ -323,9 +378,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
   for (int it = blockIdx.x; it < t.n_items; it += gridDim.x, ++iter) {
     const int s = iter % kTmaStages;
     mbar_wait(&full[s], (iter / kTmaStages) & 1);
-    const StageMeta& m = meta[s];
+    const uint4* m = meta + s * 32;
+    const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
+    const int nvcol = h->nvcol, nvec = h->nrow * h->nvcol, nt = h->nterms, no = h->nout;
+    const int ng = h->ngroups;
+    const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;
     const unsigned char* in = stage + s * kStageBytes;
-    const int nvcol = m.nvcol, nvec = m.nrow * m.nvcol, nt = m.nterms, no = m.nout;
     for (int v = ctid; v < nvec; v += nct) {
       const int r = v / nvcol;
       const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
@@ -335,11 +393,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
       } else if (nt == 1) {
         val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
       } else {
-        val = grouped_sum<T, 16>(nt, m.ngroups, m.gsize, [&](int k) {
+        val = grouped_sum<T, 16>(nt, ng, h->gsize, [&](int k) {
           return *reinterpret_cast<const uint4*>(in + (static_cast<size_t>(k) * nvec + v) * 16);
         });
       }
-      for (int o = 0; o < no; ++o) __stcs(reinterpret_cast<uint4*>(m.out[o].row0 + r * m.out[o].step + cb), val);
+      for (int o = 0; o < no; ++o) __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -498,12 +556,27 @@ cudaError_t by_dtype(int dtype, dim3 grid, dim3 block, cudaStream_t s, Args... a
   return cudaGetLastError();
 }
 
-constexpr size_t kTmaSmem = kTmaStages * kStageBytes + kTmaStages * sizeof(StageMeta) +
+constexpr size_t kTmaSmem = kTmaStages * kStageBytes + kTmaStages * 32 * sizeof(uint4) +
                             2 * kTmaStages * sizeof(uint64_t);
 
 template <class T>
 struct PhaseK {
-  static void launch(dim3 g, dim3 b, cudaStream_t s, PhaseTables t, int vb, bool tma) {
+  template <bool R>
+  static void reg(dim3 g, dim3 b, cudaStream_t s, PhaseTables t, int vb) {
+    switch (vb) {
+      case 16: box_phase_kernel<T, 16, R><<<g, b, 0, s>>>(t); break;
+      case 8:
+        if constexpr (sizeof(T) <= 8) box_phase_kernel<T, 8, R><<<g, b, 0, s>>>(t);
+        break;
+      case 4:
+        if constexpr (sizeof(T) <= 4) box_phase_kernel<T, 4, R><<<g, b, 0, s>>>(t);
+        break;
+      case 2:
+        if constexpr (sizeof(T) <= 2) box_phase_kernel<T, 2, R><<<g, b, 0, s>>>(t);
+        break;
+    }
+  }
+  static void launch(dim3 g, dim3 b, cudaStream_t s, PhaseTables t, int vb, bool tma, bool reduce) {
     if (tma) {
       static bool configured = [] {
         cudaFuncSetAttribute(box_phase_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -514,18 +587,10 @@ struct PhaseK {
       box_phase_tma_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       return;
     }
-    switch (vb) {
-      case 16: box_phase_kernel<T, 16><<<g, b, 0, s>>>(t); break;
-      case 8:
-        if constexpr (sizeof(T) <= 8) box_phase_kernel<T, 8><<<g, b, 0, s>>>(t);
-        break;
-      case 4:
-        if constexpr (sizeof(T) <= 4) box_phase_kernel<T, 4><<<g, b, 0, s>>>(t);
-        break;
-      case 2:
-        if constexpr (sizeof(T) <= 2) box_phase_kernel<T, 2><<<g, b, 0, s>>>(t);
-        break;
-    }
+    if (reduce)
+      reg<true>(g, b, s, t, vb);
+    else
+      reg<false>(g, b, s, t, vb);
   }
 };
 template <class T>
@@ -546,10 +611,10 @@ struct VerifyK {
 
 int tma_grid(int sm_count) { return sm_count; }
 
-cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, int grid,
-                         cudaStream_t s) {
+cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, bool reduce,
+                         int grid, cudaStream_t s) {
   if (t.n_items == 0) return cudaSuccess;
-  return by_dtype<PhaseK>(dtype, dim3(grid), dim3(kBlock), s, t, vec_bytes, tma);
+  return by_dtype<PhaseK>(dtype, dim3(grid), dim3(kBlock), s, t, vec_bytes, tma, reduce);
 }
 
 cudaError_t launch_fill(const FillDesc& f, int dtype, cudaStream_t s) {

@@ -48,11 +48,28 @@ struct WorkItem {
   int32_t nvcol;
 };
 
+// TMA-path item record, built on the host so the producer warp fetches one
+// fixed-size slot per item (no dependent descriptor loads):
+//   TmaRecHead, then (nterms + nout) TmaOperand: terms first, then outputs.
+struct TmaRecHead {
+  int32_t nterms, nout, ngroups, nrow;
+  int32_t nvcol, pad0, pad1, pad2;
+  uint8_t gsize[16];
+};
+struct TmaOperand {
+  char* row0;    // address of the item's first row (may be a peer address for terms)
+  int64_t step;  // bytes between rows
+};
+inline constexpr int kTmaHeadWords = sizeof(TmaRecHead) / 16;                 // 3
+inline constexpr int kTmaMaxWords = kTmaHeadWords + kMaxTerms + kMaxOuts;    // 27 <= 32 lanes
+
 struct PhaseTables {
   const TaskDesc* tasks;
   const TermDesc* terms;
-  const WorkItem* items;
+  const WorkItem* items;  // register path
+  const uint4* recs;      // TMA path: n_items slots of rec_words 16-byte words
   int32_t n_items;
+  int32_t rec_words;
 };
 
 // Shared-memory staging of the TMA kernel: kStages ring buffers of
@@ -63,8 +80,10 @@ inline constexpr int kStageBytes = 48 * 1024;
 
 // dtype codes follow hshard::DType (F32, F64, I32, I64, BF16).
 // `tma`: items were sized for the TMA pipeline (16-byte vectors only).
-cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, int grid,
-                         cudaStream_t s);
+// `reduce`: register-path items of tasks with >= 2 terms (a separate, higher
+// register-budget instantiation from the copy/zero one).
+cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, bool reduce,
+                         int grid, cudaStream_t s);
 int tma_grid(int sm_count);
 
 // Counter-hash payload generator (mirror of oracle/datagen.py).

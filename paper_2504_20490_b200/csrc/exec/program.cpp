@@ -37,6 +37,7 @@ namespace {
 constexpr int64_t kItemBytes = 64 * 1024;     // register path, output bytes per item
 constexpr int64_t kTmaItemBytes = 32 * 1024;  // TMA path upper bound (also <= stage / nterms)
 constexpr int kBlocksPerSm = 2;
+constexpr int kSlots = 9;
 
 SliceRegion bounds_only(const SliceRegion& r) {
   SliceRegion b;
@@ -476,9 +477,12 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   struct Host {
     std::vector<TaskDesc> tasks;
     std::vector<TermDesc> terms;
-    std::vector<WorkItem> items[5];  // [0] TMA, then register path by width 16, 8, 4, 2
+    // [0] TMA; [1..4] register copy/zero by width 16, 8, 4, 2; [5..8] register reduce
+    std::vector<WorkItem> items[kSlots];
   };
-  auto slot_of = [](int vb, bool tma) { return tma ? 0 : vb == 16 ? 1 : vb == 8 ? 2 : vb == 4 ? 3 : 4; };
+  auto slot_of = [](int vb, bool tma, bool reduce) {
+    return tma ? 0 : (vb == 16 ? 1 : vb == 8 ? 2 : vb == 4 ? 3 : 4) + (reduce ? 4 : 0);
+  };
   std::vector<Host> ph(n_phases_);
   stats_.phases = n_phases_;
   const int me = ctx_.rank();
@@ -582,7 +586,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     if (tma) item_bytes = std::min<int64_t>(kTmaItemBytes, kStageBytes / std::max(1, td.nterms));
     const int64_t target = std::max<int64_t>(1, item_bytes / vb);
     const int64_t planes = static_cast<int64_t>(td.n[2]) * td.n[3];
-    std::vector<WorkItem>& items = H.items[slot_of(vb, tma)];
+    std::vector<WorkItem>& items = H.items[slot_of(vb, tma, td.nterms >= 2)];
     for (int64_t pl = 0; pl < planes; ++pl) {
       if (row_vecs >= target) {
         for (int32_t r = 0; r < td.n[1]; ++r)
@@ -598,6 +602,45 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     }
   }
 
+  // TMA item records: header + every operand's first-row address, one
+  // fixed-size slot per item so the producer warp never chases descriptors.
+  std::vector<std::vector<uint4>> recs(n_phases_);
+  std::vector<int> rec_words(n_phases_, kTmaHeadWords);
+  for (int p = 0; p < n_phases_; ++p) {
+    const Host& H = ph[p];
+    for (const WorkItem& w : H.items[0]) {
+      const TaskDesc& td = H.tasks[w.task];
+      rec_words[p] = std::max(rec_words[p], kTmaHeadWords + td.nterms + td.nout);
+    }
+    const int W = rec_words[p];
+    recs[p].assign(H.items[0].size() * W, make_uint4(0, 0, 0, 0));
+    for (size_t i = 0; i < H.items[0].size(); ++i) {
+      const WorkItem& w = H.items[0][i];
+      const TaskDesc& td = H.tasks[w.task];
+      uint4* slot = recs[p].data() + i * W;
+      TmaRecHead head{};
+      head.nterms = td.nterms;
+      head.nout = td.nout;
+      head.ngroups = td.ngroups;
+      head.nrow = w.nrow;
+      head.nvcol = w.nvcol;
+      std::memcpy(head.gsize, td.gsize, sizeof(head.gsize));
+      std::memcpy(slot, &head, sizeof(head));
+      const int64_t i2 = w.plane % td.n[2], i3 = w.plane / td.n[2];
+      auto operand = [&](const TermDesc& t) {
+        TmaOperand op;
+        op.row0 = const_cast<char*>(t.base) +
+                  es_ * (w.row0 * t.stride[0] + i2 * t.stride[1] + i3 * t.stride[2]) +
+                  static_cast<int64_t>(w.vcol0) * 16;
+        op.step = t.stride[0] * es_;
+        return op;
+      };
+      TmaOperand* ops = reinterpret_cast<TmaOperand*>(slot + kTmaHeadWords);
+      for (int k = 0; k < td.nterms; ++k) ops[k] = operand(H.terms[td.term0 + k]);
+      for (int o = 0; o < td.nout; ++o) ops[td.nterms + o] = operand(H.terms[td.out0 + o]);
+    }
+  }
+
   // One device block for every phase's tables.
   size_t total = 0;
   auto reserve = [&total](size_t bytes) {
@@ -606,21 +649,23 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     return off;
   };
   struct Offs {
-    size_t tasks, terms, items[5];
+    size_t tasks, terms, items[kSlots], recs;
   };
   std::vector<Offs> offs(n_phases_);
   for (int p = 0; p < n_phases_; ++p) {
     offs[p].tasks = reserve(ph[p].tasks.size() * sizeof(TaskDesc));
     offs[p].terms = reserve(ph[p].terms.size() * sizeof(TermDesc));
-    for (int v = 0; v < 5; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
+    for (int v = 0; v < kSlots; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
+    offs[p].recs = reserve(recs[p].size() * sizeof(uint4));
   }
   std::vector<char> host(std::max<size_t>(total, 1));
   for (int p = 0; p < n_phases_; ++p) {
     std::memcpy(host.data() + offs[p].tasks, ph[p].tasks.data(), ph[p].tasks.size() * sizeof(TaskDesc));
     std::memcpy(host.data() + offs[p].terms, ph[p].terms.data(), ph[p].terms.size() * sizeof(TermDesc));
-    for (int v = 0; v < 5; ++v)
+    for (int v = 0; v < kSlots; ++v)
       std::memcpy(host.data() + offs[p].items[v], ph[p].items[v].data(),
                   ph[p].items[v].size() * sizeof(WorkItem));
+    std::memcpy(host.data() + offs[p].recs, recs[p].data(), recs[p].size() * sizeof(uint4));
   }
   cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
   cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
@@ -632,16 +677,18 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   for (int p = 0; p < n_phases_; ++p) {
     DevicePhase& d = dphases_[p];
     int64_t n = 0;
-    for (int v = 0; v < 5; ++v) {
+    for (int v = 0; v < kSlots; ++v) {
       const int32_t cnt = static_cast<int32_t>(ph[p].items[v].size());
       n += cnt;
       if (!cnt) continue;
       Launch l;
       l.tables = {reinterpret_cast<TaskDesc*>(base + offs[p].tasks),
                   reinterpret_cast<TermDesc*>(base + offs[p].terms),
-                  reinterpret_cast<WorkItem*>(base + offs[p].items[v]), cnt};
+                  reinterpret_cast<WorkItem*>(base + offs[p].items[v]),
+                  reinterpret_cast<const uint4*>(base + offs[p].recs), cnt, rec_words[p]};
       l.tma = v == 0;
-      l.vec_bytes = v <= 1 ? 16 : 16 >> (v - 1);
+      l.reduce = v >= 5;
+      l.vec_bytes = v == 0 ? 16 : 16 >> ((v - 1) % 4);
       l.grid = l.tma ? std::max(1, std::min<int>(cnt, tma_grid(ctx_.sm_count())))
                      : std::max(1, std::min<int>(cnt, max_grid));
       if (l.tma) stats_.tma_items += cnt;
@@ -671,7 +718,8 @@ void Program::run(cudaStream_t s) {
   for (int p = 0; p < n_phases_; ++p) {
     if (profiling_) event();
     for (const Launch& l : dphases_[p].launches)
-      cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.tma, l.grid, s), "box_phase launch");
+      cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s),
+                 "box_phase launch");
     if (profiling_) event();
     ctx_.barrier(s);  // phase outputs visible to every rank / inputs released
   }

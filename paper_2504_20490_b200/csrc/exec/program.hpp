@@ -135,6 +135,7 @@ class Program {
     PhaseTables tables{};
     int vec_bytes = 16;
     bool tma = false;
+    bool reduce = false;
     int grid = 1;
   };
   struct DevicePhase {
