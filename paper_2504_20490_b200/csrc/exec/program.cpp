@@ -571,7 +571,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       H.terms.push_back(tm);
       all_local = all_local && refs[k].L->rank == me;
     }
-    const bool tma = vb == 16 && all_local && !(flags_ & HS_PROG_NO_TMA);
+    const bool tma = vb == 16 && (all_local || (flags_ & HS_PROG_TMA_PEER)) && !(flags_ & HS_PROG_NO_TMA);
     const int32_t task_id = static_cast<int32_t>(H.tasks.size());
     H.tasks.push_back(td);
     stats_.tasks += 1;
@@ -698,7 +698,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }
-  const int barriers = ctx_.world() > 1 ? n_phases_ + 1 : 0;
+  const int barriers = ctx_.world() > 1 ? n_phases_ : 0;
   stats_.kernels_per_run = launches + barriers;
 }
 
@@ -714,14 +714,17 @@ void Program::run(cudaStream_t s) {
     cuda_check(cudaEventRecord(events_[events_used_], s), "cudaEventRecord");
     ++events_used_;
   };
-  ctx_.barrier(s);  // sources of every rank are ready
+  // Before each phase every rank has finished everything earlier on its
+  // stream: sources are ready, the previous phase's outputs are visible, and
+  // the previous run's readers are done (so no trailing barrier is needed;
+  // callers sync all ranks before modifying sources).
   for (int p = 0; p < n_phases_; ++p) {
+    ctx_.barrier(s);
     if (profiling_) event();
     for (const Launch& l : dphases_[p].launches)
       cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s),
                  "box_phase launch");
     if (profiling_) event();
-    ctx_.barrier(s);  // phase outputs visible to every rank / inputs released
   }
 }
 

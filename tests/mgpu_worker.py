@@ -94,7 +94,13 @@ def main():
     except Exception:
         ok = False
         results.append({"error": traceback.format_exc()})
-    print(json.dumps({"rank": rank, "ok": ok, "cases": results}), flush=True)
+    out = os.environ.get("HS_MGPU_OUT")
+    line = json.dumps({"rank": rank, "ok": ok, "cases": results})
+    if out:
+        with open(f"{out}.{rank}", "w") as f:
+            f.write(line + "\n")
+    else:
+        print(line, flush=True)
     ctx.close()
     dist.destroy_process_group()
 

@@ -26,14 +26,20 @@ def _gpus():
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-def test_multi_gpu_parity():
+@pytest.mark.parametrize("flags", ["0,14,1", "16,17"])  # 16 = TMA bulk copies from peer memory
+def test_multi_gpu_parity(tmp_path, flags):
     n = min(_gpus(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", "--master-port=29517",
+           "--master-addr=127.0.0.1", f"--master-port={29517 + len(flags)}",
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    lines = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    out = os.path.join(tmp_path, "mgpu")
+    env = dict(os.environ, HS_MGPU_OUT=out, HS_MGPU_FLAGS=flags)
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
+    lines = []
+    for r in range(n):
+        with open(f"{out}.{r}") as f:
+            lines.append(json.loads(f.read()))
     assert len(lines) == n, (res.stdout[-2000:], res.stderr[-2000:])
     for l in lines:
         assert l["ok"], json.dumps(l)[:3000]
