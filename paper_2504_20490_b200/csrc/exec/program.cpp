@@ -571,7 +571,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       H.terms.push_back(tm);
       all_local = all_local && refs[k].L->rank == me;
     }
-    const bool tma = vb == 16 && (all_local || (flags_ & HS_PROG_TMA_PEER)) && !(flags_ & HS_PROG_NO_TMA);
+    const bool tma = vb == 16 && (all_local || !(flags_ & HS_PROG_NO_TMA_PEER)) && !(flags_ & HS_PROG_NO_TMA);
     const int32_t task_id = static_cast<int32_t>(H.tasks.size());
     H.tasks.push_back(td);
     stats_.tasks += 1;

@@ -29,7 +29,7 @@ HS_PROG_FUSE_PHASES = 1   # fuse phase-1 sums into phase-2 tasks (default when w
 HS_PROG_NO_FUSE = 2       # materialise the mid annotation
 HS_PROG_NO_TMA = 4        # register path only
 HS_PROG_NO_MERGE = 8      # one task per destination shard
-HS_PROG_TMA_PEER = 16     # TMA bulk copies may read peer-GPU terms
+HS_PROG_NO_TMA_PEER = 16  # peer (NVLink) terms use the register path
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
