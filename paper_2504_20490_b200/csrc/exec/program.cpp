@@ -89,6 +89,7 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
   const bool has_mid = comm && comm->mid.has_value();
   states_.resize(has_mid ? 3 : 2);
   mid_state_ = has_mid ? 1 : -1;
+  final_state_ = states_.size() - 1;
 
   auto add_state = [&](int state, int t, const HetAnnotation& a, const size_t* offs) {
     for (const auto& [d, reg] : placements(a, shapes_[t])) {
@@ -164,6 +165,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     task.box = bounds_only(box);
     covered(tgt, t, dd, task.box, why);
     task.dsts.push_back({tgt, dd});
+    task.rank = loc(tgt, t, dd).rank;
     for (DeviceId m : from) {
       covered(src, t, m, task.box, why);
       task.terms.push_back({src, m});
@@ -283,34 +285,38 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   stats_.plan_phases = n_phases_;
 
   // ---- rewrites (results are bit-identical by construction; see header)
-  const bool fuse = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE) &&
-                    ((flags_ & HS_PROG_FUSE_PHASES) || ctx_.world() == 1);
-  if (fuse) tasks = fuse_phases(std::move(tasks));
+  const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
+  if (two_phase) {
+    // world 1: fuse everything fusable.  world > 1: relays for remote mid
+    // reads, fusion only where it adds no NVLink bytes (HS_PROG_FUSE_PHASES:
+    // fuse regardless, pulling raw inputs; HS_PROG_NO_RELAY: plain pulls).
+    if (ctx_.world() == 1 || (flags_ & HS_PROG_FUSE_PHASES))
+      tasks = fuse_phases(std::move(tasks), false);
+    else if (!(flags_ & HS_PROG_NO_RELAY))
+      tasks = fuse_phases(std::move(tasks), true);
+  }
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
-  if (!(flags_ & HS_PROG_NO_MERGE)) tasks = merge_outputs(std::move(tasks), rank_of);
+  if (!(flags_ & HS_PROG_NO_MERGE)) tasks = merge_outputs(std::move(tasks));
 
-  // Symmetric placement of the intermediate shards still materialised:
-  // every rank packs its own mid shards densely from one common base.
+  // Symmetric placement of the intermediate (mid) and relay shards still in
+  // use: every rank packs its own densely from one common base.
   if (mid_state_ >= 0) {
-    std::set<DeviceId> used_mid;
-    for (const BoxTask& t : tasks) {
-      for (const Operand& o : t.dsts)
-        if (o.state == mid_state_) used_mid.insert(o.dev);
-      for (const Operand& o : t.terms)
-        if (o.state == mid_state_) used_mid.insert(o.dev);
-    }
-    if (!used_mid.empty()) {
+    std::set<std::pair<int, DeviceId>> used_keys;  // (state, dev)
+    for (const BoxTask& t : tasks)
+      for (const auto* ops : {&t.dsts, &t.terms})
+        for (const Operand& o : *ops)
+          if (o.state >= mid_state_ && o.state != static_cast<int>(final_state_)) used_keys.insert({o.state, o.dev});
+    if (!used_keys.empty()) {
       std::vector<size_t> used(ctx_.world(), 0);
-      for (auto& [key, L] : states_[mid_state_]) {
-        if (!used_mid.count(key.second)) continue;
+      for (const auto& [st, dev] : used_keys) {
+        ShardLoc& L = states_[st].at({0, dev});
         size_t& u = used[L.rank];
         u = (u + 255) & ~size_t{255};
         L.offset = u;
         u += static_cast<size_t>(L.region.cells()) * es_;
       }
       const size_t base = ctx_.alloc(*std::max_element(used.begin(), used.end()) + 256);
-      for (auto& [key, L] : states_[mid_state_])
-        if (used_mid.count(key.second)) L.offset += base;
+      for (const auto& [st, dev] : used_keys) states_[st].at({0, dev}).offset += base;
     }
   }
 
@@ -318,24 +324,38 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   const int me = ctx_.rank();
   std::vector<BoxTask> mine;
   stats_.phase_bytes.assign(n_phases_, {0, 0, 0});
+  // My kernels: local reads / local writes / NVLink (remote reads + remote
+  // stores) per phase.  Per GPU: nvlink_in = bytes arriving (my remote reads
+  // + peers' stores into me), nvlink_out = bytes leaving.
   for (BoxTask& t : tasks) {
     const int64_t bytes = cells_of(t.box) * es_;
-    const int owner = rank_of(t.dsts.front(), t.tensor);
-    if (owner == me) {
-      auto& pb = stats_.phase_bytes[t.phase];
-      const int64_t w = bytes * static_cast<int64_t>(t.dsts.size());
-      stats_.hbm_write += w;
-      pb[1] += w;
-      for (const Operand& o : t.terms) {
-        const bool local = rank_of(o, t.tensor) == me;
-        (local ? stats_.hbm_read : stats_.nvlink_in) += bytes;
-        pb[local ? 0 : 2] += bytes;
+    const bool mine_task = t.rank == me;
+    auto& pb = stats_.phase_bytes[t.phase];
+    for (const Operand& o : t.terms) {
+      const int r = rank_of(o, t.tensor);
+      if (mine_task && r == me) {
+        stats_.hbm_read += bytes;
+        pb[0] += bytes;
+      } else if (mine_task) {
+        stats_.nvlink_in += bytes;
+        pb[2] += bytes;
+      } else if (r == me) {
+        stats_.nvlink_out += bytes;
       }
-      mine.push_back(std::move(t));
-    } else {
-      for (const Operand& o : t.terms)
-        if (rank_of(o, t.tensor) == me) stats_.nvlink_out += bytes;
     }
+    for (const Operand& o : t.dsts) {
+      const int r = rank_of(o, t.tensor);
+      if (mine_task && r == me) {
+        stats_.hbm_write += bytes;
+        pb[1] += bytes;
+      } else if (mine_task) {
+        stats_.nvlink_out += bytes;
+        pb[2] += bytes;
+      } else if (r == me) {
+        stats_.nvlink_in += bytes;
+      }
+    }
+    if (mine_task) mine.push_back(std::move(t));
   }
   for (const BoxTask& t : mine) {
     for (const Operand& o : t.dsts)
@@ -348,97 +368,155 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   build_tables(mine);
 }
 
-// ---------------------------------------------------------------- fusion
-std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks) {
-  // Producers of each mid shard (phase 0 tasks write exactly one mid operand).
+// ---------------------------------------------------------------- fusion / relays
+// Per phase-2 term reading an intermediate (mid) shard c:
+//   FUSE  -- read the phase-1 producers' inputs directly (grouped, rounded
+//            where mid would have been); needs every input on this rank at
+//            world > 1 so fusion never adds NVLink traffic;
+//   RELAY -- (world > 1, c on another rank) the phase-1 producers also store
+//            their result straight into a relay copy of c in this rank's HBM
+//            (a remote store from the reducing kernel: transfer and reduction
+//            overlap), and the phase-2 term reads it locally;
+//   KEEP  -- read the materialised mid shard.
+std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay) {
+  enum Policy { FUSE, KEEP, RELAY };
+  auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
   std::map<DeviceId, std::vector<int>> producers;
   for (int i = 0; i < static_cast<int>(tasks.size()); ++i)
     if (tasks[i].phase == 0 && tasks[i].dsts.size() == 1 && tasks[i].dsts[0].state == mid_state_)
       producers[tasks[i].dsts[0].dev].push_back(i);
 
+  int relay_state = -1;
+  auto relay_operand = [&](DeviceId c, int q) {
+    if (relay_state < 0) {
+      relay_state = static_cast<int>(states_.size());
+      states_.emplace_back();
+    }
+    const DeviceId id = c * ctx_.world() + q;
+    auto& m = states_[relay_state];
+    if (!m.count({0, id})) {
+      ShardLoc L = loc(mid_state_, 0, c);
+      L.rank = q;
+      L.offset = SIZE_MAX;
+      m[{0, id}] = L;
+    }
+    return Operand{relay_state, id};
+  };
+
   std::vector<BoxTask> out;
-  std::vector<char> needed(tasks.size(), 0);
+  std::vector<char> keep_local(tasks.size(), 0);
+  std::vector<std::set<int>> relay_to(tasks.size());
   bool any_unfused = false;
 
   for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
-    BoxTask& T = tasks[i];
+    const BoxTask& T = tasks[i];
     if (T.phase != 1) continue;
     if (T.terms.empty()) {  // zero-fill reads nothing
       out.push_back(T);
       continue;
     }
-    // Producer tasks intersecting the box, per term.
-    std::vector<std::vector<int>> prod(T.terms.size());
-    bool ok = T.groups.empty() && !T.terms.empty();
-    for (size_t j = 0; ok && j < T.terms.size(); ++j) {
-      if (T.terms[j].state != mid_state_) {
-        ok = false;
-        break;
-      }
-      for (int p : producers[T.terms[j].dev])
+    const int q = T.rank;
+    const size_t nt = T.terms.size();
+    std::vector<Policy> pol(nt, KEEP);
+    std::vector<std::vector<int>> prod(nt);
+    for (size_t j = 0; j < nt; ++j) {
+      const Operand& o = T.terms[j];
+      if (o.state != mid_state_ || !T.groups.empty()) continue;
+      bool fusable = true;
+      for (int p : producers[o.dev])
         if (intersect(tasks[p].box, T.box)) {
-          if (tasks[p].terms.empty() || !tasks[p].groups.empty()) ok = false;
           prod[j].push_back(p);
+          fusable = fusable && !tasks[p].terms.empty() && tasks[p].groups.empty();
+          if (relay)
+            for (const Operand& in : tasks[p].terms) fusable = fusable && rank_of(in, T.tensor) == q;
         }
+      if (relay && rank_of(o, T.tensor) != q)
+        pol[j] = RELAY;
+      else if (fusable && !prod[j].empty())
+        pol[j] = FUSE;
     }
-    // Grid of the box cut by every producer boundary.
-    detail::Cuts cuts(T.box.bounds.size());
-    if (ok) {
+    auto build = [&](std::vector<BoxTask>& cells) {
+      detail::Cuts cuts(T.box.bounds.size());
       for (size_t d = 0; d < cuts.size(); ++d) {
         const int64_t lo = T.box.bounds[d][0], hi = T.box.bounds[d][1];
         std::set<int64_t> s{lo, hi};
-        for (const auto& list : prod)
-          for (int p : list)
-            for (int64_t v : tasks[p].box.bounds[d])
-              if (lo < v && v < hi) s.insert(v);
+        for (size_t j = 0; j < nt; ++j)
+          if (pol[j] == FUSE)
+            for (int p : prod[j])
+              for (int64_t v : tasks[p].box.bounds[d])
+                if (lo < v && v < hi) s.insert(v);
         cuts[d].assign(s.begin(), s.end());
       }
-    }
-    std::vector<BoxTask> cells;
-    if (ok) {
+      bool ok = true;
       detail::for_each_grid_cell(cuts, [&](const SliceRegion& cell) {
         if (!ok) return;
-        BoxTask N;
-        N.phase = 1;
-        N.kind = T.kind;
-        N.tensor = T.tensor;
+        BoxTask N = T;
         N.box = cell;
-        N.dsts = T.dsts;
+        N.terms.clear();
+        N.groups.clear();
         bool nested = false;
-        for (size_t j = 0; j < T.terms.size() && ok; ++j) {
-          const BoxTask* src = nullptr;
-          for (int p : prod[j])
-            if (tasks[p].box.covers(cell)) src = &tasks[p];
-          if (!src) {
-            ok = false;
-            break;
+        for (size_t j = 0; j < nt; ++j) {
+          if (pol[j] == FUSE) {
+            const BoxTask* src = nullptr;
+            for (int p : prod[j])
+              if (tasks[p].box.covers(cell)) src = &tasks[p];
+            if (!src) {
+              ok = false;
+              return;
+            }
+            N.terms.insert(N.terms.end(), src->terms.begin(), src->terms.end());
+            N.groups.push_back(static_cast<int>(src->terms.size()));
+            nested = nested || src->terms.size() > 1;
+          } else {
+            N.terms.push_back(pol[j] == RELAY ? relay_operand(T.terms[j].dev, q) : T.terms[j]);
+            N.groups.push_back(1);
           }
-          N.terms.insert(N.terms.end(), src->terms.begin(), src->terms.end());
-          N.groups.push_back(static_cast<int>(src->terms.size()));
-          nested = nested || src->terms.size() > 1;
         }
         if (!nested) N.groups.clear();
         if (N.terms.size() > static_cast<size_t>(kMaxTerms) || N.groups.size() > 16) ok = false;
         cells.push_back(std::move(N));
       });
+      return ok;
+    };
+    std::vector<BoxTask> cells;
+    if (!build(cells)) {  // too many terms: stop fusing this task
+      for (Policy& p : pol)
+        if (p == FUSE) p = KEEP;
+      cells.clear();
+      build(cells);
     }
-    if (ok) {
-      stats_.fused_tasks += static_cast<int64_t>(cells.size());
-      for (BoxTask& c : cells) out.push_back(std::move(c));
-    } else {
+    for (size_t j = 0; j < nt; ++j) {
+      if (pol[j] == FUSE) continue;
       any_unfused = true;
-      for (const auto& list : prod)
-        for (int p : list) needed[p] = 1;
-      // unfused tasks keep reading mid: every producer of their mid shards is needed
-      for (const Operand& o : T.terms)
-        if (o.state == mid_state_)
-          for (int p : producers[o.dev]) needed[p] = 1;
-      out.push_back(T);
+      if (T.terms[j].state != mid_state_) continue;
+      for (int p : producers[T.terms[j].dev]) {
+        if (pol[j] == RELAY)
+          relay_to[p].insert(q);
+        else
+          keep_local[p] = 1;
+      }
     }
+    bool fused_any = false;
+    for (Policy p : pol) fused_any = fused_any || p == FUSE;
+    if (fused_any) stats_.fused_tasks += static_cast<int64_t>(cells.size());
+    for (BoxTask& c : cells) out.push_back(std::move(c));
   }
   std::vector<BoxTask> result;
-  for (int i = 0; i < static_cast<int>(tasks.size()); ++i)
-    if (tasks[i].phase == 0 && needed[i]) result.push_back(tasks[i]);
+  for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
+    if (tasks[i].phase != 0) continue;
+    BoxTask P = tasks[i];
+    const bool is_producer = P.dsts.size() == 1 && P.dsts[0].state == mid_state_;
+    if (is_producer) {
+      const DeviceId c = P.dsts[0].dev;
+      if (!keep_local[i]) P.dsts.clear();
+      for (int q : relay_to[i]) {
+        P.dsts.push_back(relay_operand(c, q));
+        stats_.relay_outputs += 1;
+      }
+      if (P.dsts.empty()) continue;
+    }
+    result.push_back(std::move(P));
+  }
   for (BoxTask& t : out) result.push_back(std::move(t));
   if (!any_unfused) {  // phase 0 vanished: one launch, no intermediate
     for (BoxTask& t : result) t.phase = 0;
@@ -448,13 +526,12 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks) {
 }
 
 // ---------------------------------------------------------------- output merging
-std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks,
-                                            const std::function<int(const Operand&, int)>& rank_of) {
+std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks) {
   std::map<std::string, int> index;
   std::vector<BoxTask> out;
   for (BoxTask& t : tasks) {
     std::ostringstream k;
-    k << t.phase << '|' << t.tensor << '|' << rank_of(t.dsts.front(), t.tensor) << '|';
+    k << t.phase << '|' << t.tensor << '|' << t.rank << '|';
     for (const auto& b : t.box.bounds) k << b[0] << ',' << b[1] << ';';
     k << '|';
     for (const Operand& o : t.terms) k << o.state << ':' << o.dev << ',';
@@ -750,6 +827,7 @@ std::string Program::stats_json() const {
     << ",\"outputs\":" << stats_.outputs << ",\"copy_tasks\":" << stats_.copy_tasks
     << ",\"reduce_tasks\":" << stats_.reduce_tasks << ",\"zero_tasks\":" << stats_.zero_tasks
     << ",\"tma_items\":" << stats_.tma_items << ",\"fused_tasks\":" << stats_.fused_tasks
+    << ",\"relay_outputs\":" << stats_.relay_outputs
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes

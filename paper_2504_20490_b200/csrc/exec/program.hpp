@@ -86,8 +86,9 @@ struct BoxTask {
   int phase = 0;
   StepKind kind = StepKind::Identity;
   int tensor = 0;
+  int rank = 0;                 // executing rank (its kernels run this task)
   SliceRegion box;              // logical coordinates (bounds only)
-  std::vector<Operand> dsts;    // >= 1, all on one rank
+  std::vector<Operand> dsts;    // >= 1; relay outputs may be on other ranks
   std::vector<Operand> terms;   // summation order; empty = zero-fill
   std::vector<int> groups;      // sizes; empty = flat (each term its own group)
 };
@@ -98,6 +99,7 @@ struct ProgramStats {
   int64_t tasks = 0, items = 0, terms = 0, outputs = 0;
   int64_t copy_tasks = 0, reduce_tasks = 0, zero_tasks = 0, tma_items = 0;
   int64_t fused_tasks = 0;   // phase-2 tasks that read phase-1 inputs directly
+  int64_t relay_outputs = 0; // phase-1 outputs stored into a consumer rank's relay buffer
   // Algorithmic bytes per run for THIS rank:
   int64_t hbm_read = 0;      // bytes of terms read from this GPU's HBM
   int64_t hbm_write = 0;     // bytes written to this GPU's HBM
@@ -143,9 +145,8 @@ class Program {
   };
 
   void lower(const CommPlan* comm, const SwitchPlan* sw);
-  std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks);
-  static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks,
-                                            const std::function<int(const Operand&, int)>& rank_of);
+  std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, bool relay);
+  static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
   void build_tables(const std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);
 
@@ -156,6 +157,7 @@ class Program {
   int n_virt_ = 0;
   int n_tensors_ = 1;
   int mid_state_ = -1;  // layout state index of the plan's mid annotation
+  size_t final_state_ = 0;  // layout state index of the destination
   std::vector<int> v_to_rank_;
   std::vector<Shape> shapes_;
   // layout states: 0 = src, 1 = mid (CommPlan with mid) / dst, 2 = dst
