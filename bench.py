@@ -353,6 +353,13 @@ def main():
                                                     "relay_outputs", "tma_items", "hbm_read", "hbm_write",
                                                     "nvlink_in", "nvlink_out", "kernels_per_run")},
                     "flags": args.flags}
+            if world > 1:
+                import torch.distributed as dist
+                per = [None] * world
+                dist.all_gather_object(per, {"phase_ms": sph, "hbm_read": sst["hbm_read"],
+                                             "hbm_write": sst["hbm_write"], "nvlink_in": sst["nvlink_in"],
+                                             "nvlink_out": sst["nvlink_out"], "items": sst["items"]})
+                line["ranks"] = per
             if rank == 0:
                 print(json.dumps(line), flush=True)
             del sprog, slay

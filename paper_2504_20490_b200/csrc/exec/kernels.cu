@@ -344,17 +344,38 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
   if (warp == 0) {
     // ---- producer warp: the item record is prefetched one item ahead (one
     // 16-byte word per lane); lane k then streams term k's rows.
-    int iter = 0;
-    int it = blockIdx.x;
+    // Items are handed out dynamically (one atomic per item, fetched one item
+    // ahead together with its record), so CTAs that draw cheap (local) items
+    // keep pulling work while others wait on NVLink.
+    const unsigned full_mask = 0xffffffffu;
+    int it = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
+    it = __shfl_sync(full_mask, it, 0);
     uint4 next = make_uint4(0, 0, 0, 0);
     if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
-    for (; it < t.n_items; it += gridDim.x, ++iter) {
+    for (int iter = 0;; ++iter) {
+      const int cur_it = it;
       const uint4 cur = next;
-      const int nit = it + gridDim.x;
-      if (nit < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nit) * W + lane];
+      if (cur_it < t.n_items) {
+        int nxt = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
+        nxt = __shfl_sync(full_mask, nxt, 0);
+        it = nxt;
+        if (nxt < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nxt) * W + lane];
+      }
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
       uint4* m = meta + s * 32;
+      if (cur_it >= t.n_items) {  // end marker for the consumers
+        if (lane == 0) {
+          reinterpret_cast<TmaRecHead*>(m)->nterms = -1;
+          mbar_arrive_expect_tx(&full[s], 0);
+          // the last CTA out resets the scheduler for the next launch
+          if (atomicAdd(&t.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+            t.sched[0] = 0;
+            t.sched[1] = 0;
+          }
+        }
+        return;
+      }
       if (lane < W) m[lane] = cur;
       __syncwarp();
       const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
@@ -368,18 +389,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
         for (int r = 0; r < nrow; ++r) bulk_g2s(dst + r * row_bytes, op.row0 + r * op.step, row_bytes, &full[s]);
       }
     }
-    return;
   }
 
   // ---- consumers
   const int ctid = threadIdx.x - 32;
   constexpr int nct = kTmaThreads - 32;
-  int iter = 0;
-  for (int it = blockIdx.x; it < t.n_items; it += gridDim.x, ++iter) {
+  for (int iter = 0;; ++iter) {
     const int s = iter % kTmaStages;
     mbar_wait(&full[s], (iter / kTmaStages) & 1);
     const uint4* m = meta + s * 32;
     const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
+    if (h->nterms < 0) break;  // producer's end marker
     const int nvcol = h->nvcol, nvec = h->nrow * h->nvcol, nt = h->nterms, no = h->nout;
     const int ng = h->ngroups;
     const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;

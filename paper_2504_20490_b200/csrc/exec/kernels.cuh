@@ -68,6 +68,7 @@ struct PhaseTables {
   const TermDesc* terms;
   const WorkItem* items;  // register path
   const uint4* recs;      // TMA path: n_items slots of rec_words 16-byte words
+  int* sched;             // TMA path: {next item, finished CTAs}; zero between launches
   int32_t n_items;
   int32_t rec_words;
 };

@@ -726,7 +726,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     return off;
   };
   struct Offs {
-    size_t tasks, terms, items[kSlots], recs;
+    size_t tasks, terms, items[kSlots], recs, sched;
   };
   std::vector<Offs> offs(n_phases_);
   for (int p = 0; p < n_phases_; ++p) {
@@ -734,6 +734,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     offs[p].terms = reserve(ph[p].terms.size() * sizeof(TermDesc));
     for (int v = 0; v < kSlots; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
     offs[p].recs = reserve(recs[p].size() * sizeof(uint4));
+    offs[p].sched = reserve(2 * sizeof(int));  // zero-initialised scheduler words
   }
   std::vector<char> host(std::max<size_t>(total, 1));
   for (int p = 0; p < n_phases_; ++p) {
@@ -762,7 +763,8 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables = {reinterpret_cast<TaskDesc*>(base + offs[p].tasks),
                   reinterpret_cast<TermDesc*>(base + offs[p].terms),
                   reinterpret_cast<WorkItem*>(base + offs[p].items[v]),
-                  reinterpret_cast<const uint4*>(base + offs[p].recs), cnt, rec_words[p]};
+                  reinterpret_cast<const uint4*>(base + offs[p].recs),
+                  reinterpret_cast<int*>(base + offs[p].sched), cnt, rec_words[p]};
       l.tma = v == 0;
       l.reduce = v >= 5;
       l.vec_bytes = v == 0 ? 16 : 16 >> ((v - 1) % 4);
