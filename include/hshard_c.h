@@ -110,7 +110,8 @@ enum {
   HS_PROG_NO_TMA = 4,      /* register path only (A/B measurements) */
   HS_PROG_NO_MERGE = 8,    /* one task per destination shard (no multi-output tasks) */
   HS_PROG_NO_TMA_PEER = 16, /* peer-GPU (NVLink) terms use the register path, not TMA */
-  HS_PROG_NO_RELAY = 32     /* world > 1: phase 2 pulls remote mid boxes (no relay stores) */
+  HS_PROG_NO_RELAY = 32,    /* world > 1: phase 2 pulls remote mid boxes (no relay stores) */
+  HS_PROG_NO_REPLICA = 64   /* world > 1: read every term from the device the plan names */
 };
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);

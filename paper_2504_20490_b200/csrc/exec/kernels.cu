@@ -344,20 +344,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
   if (warp == 0) {
     // ---- producer warp: the item record is prefetched one item ahead (one
     // 16-byte word per lane); lane k then streams term k's rows.
-    // Items are handed out dynamically (one atomic per item, fetched one item
-    // ahead together with its record), so CTAs that draw cheap (local) items
-    // keep pulling work while others wait on NVLink.
+    // Items [0, n_static) are dealt round-robin (no dependency: the record is
+    // prefetched one item ahead); the tail is handed out dynamically (one
+    // atomic per item) so CTAs that drew cheap items keep pulling work.
     const unsigned full_mask = 0xffffffffu;
-    int it = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
-    it = __shfl_sync(full_mask, it, 0);
+    auto next_item = [&](int prev, int iter_next) {
+      const int st = blockIdx.x + iter_next * static_cast<int>(gridDim.x);
+      if (st < t.n_static) return st;
+      int d = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
+      return t.n_static + __shfl_sync(full_mask, d, 0);
+    };
+    int it = next_item(-1, 0);
     uint4 next = make_uint4(0, 0, 0, 0);
     if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
     for (int iter = 0;; ++iter) {
       const int cur_it = it;
       const uint4 cur = next;
       if (cur_it < t.n_items) {
-        int nxt = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
-        nxt = __shfl_sync(full_mask, nxt, 0);
+        const int nxt = next_item(cur_it, iter + 1);
         it = nxt;
         if (nxt < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nxt) * W + lane];
       }

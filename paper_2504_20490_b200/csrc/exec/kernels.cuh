@@ -71,6 +71,7 @@ struct PhaseTables {
   int* sched;             // TMA path: {next item, finished CTAs}; zero between launches
   int32_t n_items;
   int32_t rec_words;
+  int32_t n_static;       // TMA path: items [0, n_static) are dealt round-robin
 };
 
 // Shared-memory staging of the TMA kernel: kStages ring buffers of

@@ -99,6 +99,8 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
       L.region = reg;
       L.rank = v_to_rank_[d];
       L.offset = offs ? offs[static_cast<size_t>(t) * n_virt_ + d] : SIZE_MAX;
+      L.subgroup = a.subgroup_of(d);
+      L.eff_hdim = a.effective_hdim();
       states_[state][{t, d}] = L;
     }
   };
@@ -285,6 +287,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   stats_.plan_phases = n_phases_;
 
   // ---- rewrites (results are bit-identical by construction; see header)
+  if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
   if (two_phase) {
     // world 1: fuse everything fusable.  world > 1: relays for remote mid
@@ -366,6 +369,48 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
         fail(Errc::MissingShard, "source shard of device " + std::to_string(o.dev) + " has no buffer");
   }
   build_tables(mine);
+}
+
+// ---------------------------------------------------------------- replicas
+// A term may be read from any device holding the SAME VALUES on its box: the
+// same bottom partial piece, the same top-tier piece (subgroup, when the top
+// tier is Partial), and -- when that piece is a partial (P > 1) -- the same
+// subgroup, since subgroups of an hdim -1 annotation may decompose the value
+// differently.  Duplicate replicas of a valid state are bit-identical
+// (reassemble's precondition), so results do not change
+// (SURVEY App. B7).  Policy: a replica on the executing rank if any, else the
+// one whose rank has served the fewest bytes so far.
+void Program::choose_replicas(std::vector<BoxTask>& tasks) {
+  std::vector<int64_t> egress(ctx_.world(), 0);
+  for (BoxTask& t : tasks) {
+    const int64_t bytes = t.box.cells() * es_;
+    for (Operand& o : t.terms) {
+      const ShardLoc& cur = loc(o.state, t.tensor, o.dev);
+      if (cur.rank == t.rank) continue;
+      DeviceId best = o.dev;
+      int best_rank = cur.rank;
+      for (const auto& [key, L] : states_[o.state]) {
+        if (key.first != t.tensor || key.second == o.dev) continue;
+        const bool same = L.region.covers(t.box) &&
+                          L.region.partial_index == cur.region.partial_index &&
+                          L.region.partial_count == cur.region.partial_count &&
+                          (cur.eff_hdim != kPartial || L.subgroup == cur.subgroup) &&
+                          (cur.region.partial_count == 1 || L.subgroup == cur.subgroup);
+        if (!same) continue;
+        const bool better = (L.rank == t.rank && best_rank != t.rank) ||
+                            (best_rank != t.rank && L.rank != t.rank && egress[L.rank] < egress[best_rank]);
+        if (better) {
+          best = key.second;
+          best_rank = L.rank;
+        }
+      }
+      if (best != o.dev) {
+        o.dev = best;
+        stats_.replica_swaps += 1;
+      }
+      if (best_rank != t.rank) egress[best_rank] += bytes;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- fusion / relays
@@ -764,13 +809,17 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
                   reinterpret_cast<TermDesc*>(base + offs[p].terms),
                   reinterpret_cast<WorkItem*>(base + offs[p].items[v]),
                   reinterpret_cast<const uint4*>(base + offs[p].recs),
-                  reinterpret_cast<int*>(base + offs[p].sched), cnt, rec_words[p]};
+                  reinterpret_cast<int*>(base + offs[p].sched), cnt, rec_words[p], 0};
       l.tma = v == 0;
       l.reduce = v >= 5;
       l.vec_bytes = v == 0 ? 16 : 16 >> ((v - 1) % 4);
       l.grid = l.tma ? std::max(1, std::min<int>(cnt, tma_grid(ctx_.sm_count())))
                      : std::max(1, std::min<int>(cnt, max_grid));
-      if (l.tma) stats_.tma_items += cnt;
+      if (l.tma) {
+        stats_.tma_items += cnt;
+        // static round-robin for the first ~3/4 of the items, dynamic tail
+        l.tables.n_static = static_cast<int32_t>((static_cast<int64_t>(cnt) * 3 / 4) / l.grid * l.grid);
+      }
       d.launches.push_back(l);
       ++launches;
     }
@@ -829,7 +878,7 @@ std::string Program::stats_json() const {
     << ",\"outputs\":" << stats_.outputs << ",\"copy_tasks\":" << stats_.copy_tasks
     << ",\"reduce_tasks\":" << stats_.reduce_tasks << ",\"zero_tasks\":" << stats_.zero_tasks
     << ",\"tma_items\":" << stats_.tma_items << ",\"fused_tasks\":" << stats_.fused_tasks
-    << ",\"relay_outputs\":" << stats_.relay_outputs
+    << ",\"relay_outputs\":" << stats_.relay_outputs << ",\"replica_swaps\":" << stats_.replica_swaps
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes

@@ -70,6 +70,8 @@ struct ShardLoc {
   SliceRegion region;
   int rank = -1;
   size_t offset = SIZE_MAX;  // arena byte offset on `rank`
+  int subgroup = 0;          // annotation subgroup of the device
+  int eff_hdim = -1;         // effective hdim of the annotation
 };
 
 // A shard in a layout state: (state, virtual device); the tensor is the task's.
@@ -100,6 +102,7 @@ struct ProgramStats {
   int64_t copy_tasks = 0, reduce_tasks = 0, zero_tasks = 0, tma_items = 0;
   int64_t fused_tasks = 0;   // phase-2 tasks that read phase-1 inputs directly
   int64_t relay_outputs = 0; // phase-1 outputs stored into a consumer rank's relay buffer
+  int64_t replica_swaps = 0; // remote terms re-sourced from a bit-identical replica
   // Algorithmic bytes per run for THIS rank:
   int64_t hbm_read = 0;      // bytes of terms read from this GPU's HBM
   int64_t hbm_write = 0;     // bytes written to this GPU's HBM
@@ -146,6 +149,7 @@ class Program {
 
   void lower(const CommPlan* comm, const SwitchPlan* sw);
   std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, bool relay);
+  void choose_replicas(std::vector<BoxTask>& tasks);
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
   void build_tables(const std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);

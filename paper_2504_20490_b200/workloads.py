@@ -193,8 +193,20 @@ def all_workloads() -> List[Workload]:
     return ws
 
 
+def link_probes() -> List[Workload]:
+    """Not BASELINE configs: 1 GiB SendRecv between two virtual devices, one
+    direction (p2p_uni: device 1 -> 0) or both (p2p_bi), to measure the NVLink
+    transport in isolation at N = 2."""
+    shape = (16384, 32768)
+    uni = Workload("p2p_uni", "classify", "bf16", 2,
+                   [(0, single([1], "{}"), single([0], "{}"), shape)])
+    bi = Workload("p2p_bi", "classify", "bf16", 2,
+                  [(0, single([0, 1], "{0:2}"), single([1, 0], "{0:2}"), shape)])
+    return [uni, bi]
+
+
 def by_name(name: str) -> Workload:
-    for w in all_workloads():
+    for w in all_workloads() + link_probes():
         if w.name == name:
             return w
     raise KeyError(name)
