@@ -450,7 +450,8 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
 
   std::vector<BoxTask> out;
   std::vector<char> keep_local(tasks.size(), 0);
-  std::vector<std::set<int>> relay_to(tasks.size());
+  // producer -> consumer rank -> boxes that rank actually reads
+  std::vector<std::map<int, std::vector<SliceRegion>>> relay_to(tasks.size());
   bool any_unfused = false;
 
   for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
@@ -535,10 +536,11 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
       any_unfused = true;
       if (T.terms[j].state != mid_state_) continue;
       for (int p : producers[T.terms[j].dev]) {
-        if (pol[j] == RELAY)
-          relay_to[p].insert(q);
-        else
+        if (pol[j] != RELAY) {
           keep_local[p] = 1;
+        } else if (auto need = intersect(tasks[p].box, T.box)) {
+          relay_to[p][q].push_back(*need);
+        }
       }
     }
     bool fused_any = false;
@@ -549,18 +551,40 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
   std::vector<BoxTask> result;
   for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
     if (tasks[i].phase != 0) continue;
-    BoxTask P = tasks[i];
+    const BoxTask& P = tasks[i];
     const bool is_producer = P.dsts.size() == 1 && P.dsts[0].state == mid_state_;
-    if (is_producer) {
-      const DeviceId c = P.dsts[0].dev;
-      if (!keep_local[i]) P.dsts.clear();
-      for (int q : relay_to[i]) {
-        P.dsts.push_back(relay_operand(c, q));
-        stats_.relay_outputs += 1;
-      }
-      if (P.dsts.empty()) continue;
+    if (!is_producer || relay_to[i].empty()) {
+      if (!is_producer || keep_local[i]) result.push_back(P);
+      continue;
     }
-    result.push_back(std::move(P));
+    // Split the producer along the boxes remote consumers read, so each
+    // piece is stored exactly where it is consumed (and locally if needed).
+    const DeviceId c = P.dsts[0].dev;
+    detail::Cuts cuts(P.box.bounds.size());
+    for (size_t d = 0; d < cuts.size(); ++d) {
+      const int64_t lo = P.box.bounds[d][0], hi = P.box.bounds[d][1];
+      std::set<int64_t> s{lo, hi};
+      for (const auto& [q, boxes] : relay_to[i])
+        for (const SliceRegion& b : boxes)
+          for (int64_t v : b.bounds[d])
+            if (lo < v && v < hi) s.insert(v);
+      cuts[d].assign(s.begin(), s.end());
+    }
+    detail::for_each_grid_cell(cuts, [&](const SliceRegion& cell) {
+      BoxTask piece = P;
+      piece.box = cell;
+      piece.dsts.clear();
+      if (keep_local[i]) piece.dsts.push_back(P.dsts[0]);
+      for (const auto& [q, boxes] : relay_to[i]) {
+        bool read = false;
+        for (const SliceRegion& b : boxes) read = read || b.covers(cell);
+        if (read) {
+          piece.dsts.push_back(relay_operand(c, q));
+          stats_.relay_outputs += 1;
+        }
+      }
+      if (!piece.dsts.empty()) result.push_back(std::move(piece));
+    });
   }
   for (BoxTask& t : out) result.push_back(std::move(t));
   if (!any_unfused) {  // phase 0 vanished: one launch, no intermediate
@@ -817,8 +841,8 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
                      : std::max(1, std::min<int>(cnt, max_grid));
       if (l.tma) {
         stats_.tma_items += cnt;
-        // static round-robin for the first ~3/4 of the items, dynamic tail
-        l.tables.n_static = static_cast<int32_t>((static_cast<int64_t>(cnt) * 3 / 4) / l.grid * l.grid);
+        // static round-robin for the first ~15/16 of the items, dynamic tail
+        l.tables.n_static = static_cast<int32_t>((static_cast<int64_t>(cnt) * 15 / 16) / l.grid * l.grid);
       }
       d.launches.push_back(l);
       ++launches;
