@@ -111,7 +111,9 @@ enum {
   HS_PROG_NO_MERGE = 8,    /* one task per destination shard (no multi-output tasks) */
   HS_PROG_NO_TMA_PEER = 16, /* peer-GPU (NVLink) terms use the register path, not TMA */
   HS_PROG_NO_RELAY = 32,    /* world > 1: phase 2 pulls remote mid boxes (no relay stores) */
-  HS_PROG_NO_REPLICA = 64   /* world > 1: read every term from the device the plan names */
+  HS_PROG_NO_REPLICA = 64,  /* world > 1: read every term from the device the plan names */
+  HS_PROG_NO_SHARE = 128,   /* world > 1: identical tasks on several ranks are not chunked */
+  HS_PROG_PULL_COPIES = 256 /* world > 1: copies run on the destination's rank (pull) */
 };
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);

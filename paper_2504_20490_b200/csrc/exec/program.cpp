@@ -299,6 +299,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
       tasks = fuse_phases(std::move(tasks), true);
   }
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
+  if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) tasks = spread_shared(std::move(tasks));
   if (!(flags_ & HS_PROG_NO_MERGE)) tasks = merge_outputs(std::move(tasks));
 
   // Symmetric placement of the intermediate (mid) and relay shards still in
@@ -481,6 +482,14 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
       else if (fusable && !prod[j].empty())
         pol[j] = FUSE;
     }
+    // world > 1: a task that waits for a relay anyway keeps its local groups
+    // in phase 1's producers (they run concurrently with the remote ones)
+    // instead of redoing them after the barrier.
+    bool needs_relay = false;
+    for (Policy p : pol) needs_relay = needs_relay || p == RELAY;
+    if (relay && needs_relay)
+      for (Policy& p : pol)
+        if (p == FUSE) p = KEEP;
     auto build = [&](std::vector<BoxTask>& cells) {
       detail::Cuts cuts(T.box.bounds.size());
       for (size_t d = 0; d < cuts.size(); ++d) {
@@ -543,9 +552,16 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
         }
       }
     }
-    bool fused_any = false;
-    for (Policy p : pol) fused_any = fused_any || p == FUSE;
+    bool fused_any = false, all_fused = true;
+    for (Policy p : pol) {
+      fused_any = fused_any || p == FUSE;
+      all_fused = all_fused && p == FUSE;
+    }
     if (fused_any) stats_.fused_tasks += static_cast<int64_t>(cells.size());
+    // A fully fused task reads only phase-1 inputs: at world > 1 it runs in
+    // phase 1 (before the barrier) alongside the producers.
+    if (relay && all_fused)
+      for (BoxTask& c : cells) c.phase = 0;
     for (BoxTask& c : cells) out.push_back(std::move(c));
   }
   std::vector<BoxTask> result;
@@ -587,11 +603,82 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
     });
   }
   for (BoxTask& t : out) result.push_back(std::move(t));
-  if (!any_unfused) {  // phase 0 vanished: one launch, no intermediate
+  bool any_late = false;
+  for (const BoxTask& t : result) any_late = any_late || t.phase == 1;
+  if (!any_unfused || !any_late) {  // one phase left: one launch, no barrier between
     for (BoxTask& t : result) t.phase = 0;
     n_phases_ = 1;
   }
   return result;
+}
+
+// ---------------------------------------------------------------- cross-rank sharing
+// world > 1: tasks that compute the same values (same phase, tensor, box,
+// inputs, groups) on several ranks -- AllReduce members, SplitAllReduce /
+// SplitAllGather receivers, replicas of one shard -- are cut into one chunk
+// per rank along the box's outermost splittable dim; each rank computes its
+// chunk once and stores it to every output (local or over NVLink).  A
+// reduce-scatter + all-gather, with the inputs of each chunk read once.
+// Then single-input copies run on the rank that holds the input (push:
+// posted NVLink stores instead of round-trip reads).
+std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
+  auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
+  std::map<std::string, std::vector<int>> same;
+  std::vector<std::string> order;
+  for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
+    const BoxTask& t = tasks[i];
+    std::ostringstream k;
+    k << t.phase << '|' << t.tensor << '|';
+    for (const auto& b : t.box.bounds) k << b[0] << ',' << b[1] << ';';
+    k << '|';
+    for (const Operand& o : t.terms) k << o.state << ':' << o.dev << ',';
+    k << '|';
+    for (int g : t.groups) k << g << ',';
+    auto [it, fresh] = same.try_emplace(k.str());
+    if (fresh) order.push_back(k.str());
+    it->second.push_back(i);
+  }
+  std::vector<BoxTask> out;
+  for (const std::string& key : order) {
+    const std::vector<int>& idx = same[key];
+    std::set<int> ranks;
+    std::vector<Operand> dsts;
+    for (int i : idx) {
+      ranks.insert(tasks[i].rank);
+      for (const Operand& o : tasks[i].dsts)
+        if (std::find(dsts.begin(), dsts.end(), o) == dsts.end()) dsts.push_back(o);
+    }
+    const BoxTask& T = tasks[idx.front()];
+    int split = -1;
+    for (size_t d = 0; d < T.box.bounds.size() && split < 0; ++d)
+      if (T.box.bounds[d][1] - T.box.bounds[d][0] >= static_cast<int64_t>(ranks.size())) split = static_cast<int>(d);
+    if (ranks.size() < 2 || dsts.size() > static_cast<size_t>(kMaxOuts) || T.terms.empty() || split < 0) {
+      for (int i : idx) out.push_back(tasks[i]);
+      continue;
+    }
+    const int64_t lo = T.box.bounds[split][0], ext = T.box.bounds[split][1] - lo;
+    const int R = static_cast<int>(ranks.size());
+    int c = 0;
+    for (int r : ranks) {
+      BoxTask chunk = T;
+      chunk.rank = r;
+      chunk.dsts = dsts;
+      chunk.box.bounds[split] = {lo + ext * c / R, lo + ext * (c + 1) / R};
+      ++c;
+      stats_.shared_chunks += 1;
+      out.push_back(std::move(chunk));
+    }
+  }
+  if (!(flags_ & HS_PROG_PULL_COPIES))
+    for (BoxTask& t : out)
+      if (t.terms.size() == 1) {
+        const int src = rank_of(t.terms[0], t.tensor);
+        if (src != t.rank) {
+          t.rank = src;
+          stats_.pushed_copies += 1;
+        }
+      }
+  return out;
 }
 
 // ---------------------------------------------------------------- output merging
@@ -903,6 +990,7 @@ std::string Program::stats_json() const {
     << ",\"reduce_tasks\":" << stats_.reduce_tasks << ",\"zero_tasks\":" << stats_.zero_tasks
     << ",\"tma_items\":" << stats_.tma_items << ",\"fused_tasks\":" << stats_.fused_tasks
     << ",\"relay_outputs\":" << stats_.relay_outputs << ",\"replica_swaps\":" << stats_.replica_swaps
+    << ",\"shared_chunks\":" << stats_.shared_chunks << ",\"pushed_copies\":" << stats_.pushed_copies
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes

@@ -103,6 +103,8 @@ struct ProgramStats {
   int64_t fused_tasks = 0;   // phase-2 tasks that read phase-1 inputs directly
   int64_t relay_outputs = 0; // phase-1 outputs stored into a consumer rank's relay buffer
   int64_t replica_swaps = 0; // remote terms re-sourced from a bit-identical replica
+  int64_t shared_chunks = 0; // per-rank chunks of tasks shared across ranks
+  int64_t pushed_copies = 0; // copies executed on the source's rank (remote stores)
   // Algorithmic bytes per run for THIS rank:
   int64_t hbm_read = 0;      // bytes of terms read from this GPU's HBM
   int64_t hbm_write = 0;     // bytes written to this GPU's HBM
@@ -150,6 +152,7 @@ class Program {
   void lower(const CommPlan* comm, const SwitchPlan* sw);
   std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, bool relay);
   void choose_replicas(std::vector<BoxTask>& tasks);
+  std::vector<BoxTask> spread_shared(std::vector<BoxTask> tasks);
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
   void build_tables(const std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);

@@ -32,6 +32,8 @@ HS_PROG_NO_MERGE = 8      # one task per destination shard
 HS_PROG_NO_TMA_PEER = 16  # peer (NVLink) terms use the register path
 HS_PROG_NO_RELAY = 32      # world > 1: pull remote mid boxes instead of relay stores
 HS_PROG_NO_REPLICA = 64    # world > 1: no replica-aware source choice
+HS_PROG_NO_SHARE = 128     # world > 1: no cross-rank chunking of identical tasks
+HS_PROG_PULL_COPIES = 256  # world > 1: copies pull (run on the destination's rank)
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
