@@ -289,18 +289,43 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   // ---- rewrites (results are bit-identical by construction; see header)
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
-  if (two_phase) {
-    // world 1: fuse everything fusable.  world > 1: relays for remote mid
-    // reads, fusion only where it adds no NVLink bytes (HS_PROG_FUSE_PHASES:
-    // fuse regardless, pulling raw inputs; HS_PROG_NO_RELAY: plain pulls).
-    if (ctx_.world() == 1 || (flags_ & HS_PROG_FUSE_PHASES))
-      tasks = fuse_phases(std::move(tasks), false);
-    else if (!(flags_ & HS_PROG_NO_RELAY))
-      tasks = fuse_phases(std::move(tasks), true);
-  }
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
-  if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) tasks = spread_shared(std::move(tasks));
-  if (!(flags_ & HS_PROG_NO_MERGE)) tasks = merge_outputs(std::move(tasks));
+  auto finish = [&](std::vector<BoxTask> ts) {
+    if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) ts = spread_shared(std::move(ts));
+    if (!(flags_ & HS_PROG_NO_MERGE)) ts = merge_outputs(std::move(ts));
+    return ts;
+  };
+  if (two_phase && (ctx_.world() == 1 || (flags_ & HS_PROG_FUSE_PHASES))) {
+    // world 1: fuse everything fusable (HS_PROG_FUSE_PHASES forces it at
+    // world > 1, pulling raw inputs over NVLink)
+    tasks = finish(fuse_phases(std::move(tasks), RelayMode::None));
+  } else if (two_phase && !(flags_ & HS_PROG_NO_RELAY)) {
+    // world > 1: relays for remote mid reads.  Whether a task that waits for
+    // a relay should also fuse its local groups (less HBM traffic, but done
+    // after the barrier) or keep them in phase 1 (concurrent with the remote
+    // producers) depends on the plan: build both, keep the cheaper by the
+    // per-rank HBM / NVLink byte model.
+    const int phases0 = n_phases_;
+    const ProgramStats stats0 = stats_;
+    std::vector<BoxTask> a = finish(fuse_phases(tasks, RelayMode::KeepLocal));
+    const int phases_a = n_phases_;
+    const ProgramStats stats_a = stats_;
+    n_phases_ = phases0;
+    stats_ = stats0;
+    std::vector<BoxTask> b = finish(fuse_phases(std::move(tasks), RelayMode::FuseLocal));
+    const double ca = estimate_seconds(a, phases_a), cb = estimate_seconds(b, n_phases_);
+    if (ca <= cb) {
+      tasks = std::move(a);
+      n_phases_ = phases_a;
+      stats_ = stats_a;
+    } else {
+      tasks = std::move(b);
+    }
+    stats_.model_ms[0] = ca * 1e3;
+    stats_.model_ms[1] = cb * 1e3;
+  } else {
+    tasks = finish(std::move(tasks));
+  }
 
   // Symmetric placement of the intermediate (mid) and relay shards still in
   // use: every rank packs its own densely from one common base.
@@ -323,6 +348,11 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
       for (const auto& [st, dev] : used_keys) states_[st].at({0, dev}).offset += base;
     }
   }
+
+  for (const BoxTask& t : tasks)
+    if (t.phase == n_phases_ - 1)
+      for (const Operand& o : t.dsts)
+        remote_final_writes_ = remote_final_writes_ || rank_of(o, t.tensor) != t.rank;
 
   // ---- algorithmic byte accounting over ALL ranks' tasks, then keep ours
   const int me = ctx_.rank();
@@ -424,7 +454,8 @@ void Program::choose_replicas(std::vector<BoxTask>& tasks) {
 //            (a remote store from the reducing kernel: transfer and reduction
 //            overlap), and the phase-2 term reads it locally;
 //   KEEP  -- read the materialised mid shard.
-std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay) {
+std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode mode) {
+  const bool relay = mode != RelayMode::None;
   enum Policy { FUSE, KEEP, RELAY };
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
   std::map<DeviceId, std::vector<int>> producers;
@@ -487,7 +518,7 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
     // instead of redoing them after the barrier.
     bool needs_relay = false;
     for (Policy p : pol) needs_relay = needs_relay || p == RELAY;
-    if (relay && needs_relay)
+    if (mode == RelayMode::KeepLocal && needs_relay)
       for (Policy& p : pol)
         if (p == FUSE) p = KEEP;
     auto build = [&](std::vector<BoxTask>& cells) {
@@ -610,6 +641,47 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, bool relay
     n_phases_ = 1;
   }
   return result;
+}
+
+// ---------------------------------------------------------------- cost model
+// Seconds for a task list: per phase, the slowest rank's max of HBM bytes /
+// 6.3 TB/s, NVLink-in / 0.7 TB/s and NVLink-out / 0.7 TB/s (peer reads are
+// served by the owner's HBM and leave through its links), plus one barrier
+// per phase.  Only used to choose between equivalent rewrites.
+double Program::estimate_seconds(const std::vector<BoxTask>& tasks, int phases) {
+  struct Load {
+    double hbm = 0, in = 0, out = 0;
+  };
+  const int W = ctx_.world();
+  std::vector<std::vector<Load>> load(phases, std::vector<Load>(W));
+  for (const BoxTask& t : tasks) {
+    const double bytes = static_cast<double>(t.box.cells()) * es_;
+    auto& L = load.at(t.phase);
+    const int r = t.rank;
+    for (const Operand& o : t.terms) {
+      const int ro = loc(o.state, t.tensor, o.dev).rank;
+      L[ro].hbm += bytes;
+      if (ro != r) {
+        L[r].in += bytes;
+        L[ro].out += bytes;
+      }
+    }
+    for (const Operand& o : t.dsts) {
+      const int ro = loc(o.state, t.tensor, o.dev).rank;
+      L[ro].hbm += bytes;
+      if (ro != r) {
+        L[r].out += bytes;
+        L[ro].in += bytes;
+      }
+    }
+  }
+  double total = 0;
+  for (const auto& per : load) {
+    double worst = 0;
+    for (const Load& l : per) worst = std::max({worst, l.hbm / 6.3e12, l.in / 7.0e11, l.out / 7.0e11});
+    total += worst + 8e-6;
+  }
+  return total;
 }
 
 // ---------------------------------------------------------------- cross-rank sharing
@@ -937,7 +1009,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }
-  const int barriers = ctx_.world() > 1 ? n_phases_ : 0;
+  const int barriers = ctx_.world() > 1 ? n_phases_ + (remote_final_writes_ ? 1 : 0) : 0;
   stats_.kernels_per_run = launches + barriers;
 }
 
@@ -955,8 +1027,10 @@ void Program::run(cudaStream_t s) {
   };
   // Before each phase every rank has finished everything earlier on its
   // stream: sources are ready, the previous phase's outputs are visible, and
-  // the previous run's readers are done (so no trailing barrier is needed;
-  // callers sync all ranks before modifying sources).
+  // the previous run's readers are done.  A program whose kernels store into
+  // peers' destination shards ends with one more barrier, so a rank's own
+  // destinations are complete when its stream is (callers still sync all
+  // ranks before modifying sources).
   for (int p = 0; p < n_phases_; ++p) {
     ctx_.barrier(s);
     if (profiling_) event();
@@ -965,6 +1039,7 @@ void Program::run(cudaStream_t s) {
                  "box_phase launch");
     if (profiling_) event();
   }
+  if (remote_final_writes_) ctx_.barrier(s);
 }
 
 void Program::run_host(const void* const* src_host, void* const* dst_host) {
@@ -991,6 +1066,7 @@ std::string Program::stats_json() const {
     << ",\"tma_items\":" << stats_.tma_items << ",\"fused_tasks\":" << stats_.fused_tasks
     << ",\"relay_outputs\":" << stats_.relay_outputs << ",\"replica_swaps\":" << stats_.replica_swaps
     << ",\"shared_chunks\":" << stats_.shared_chunks << ",\"pushed_copies\":" << stats_.pushed_copies
+    << ",\"model_ms\":[" << stats_.model_ms[0] << "," << stats_.model_ms[1] << "]"
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes

@@ -105,6 +105,7 @@ struct ProgramStats {
   int64_t replica_swaps = 0; // remote terms re-sourced from a bit-identical replica
   int64_t shared_chunks = 0; // per-rank chunks of tasks shared across ranks
   int64_t pushed_copies = 0; // copies executed on the source's rank (remote stores)
+  double model_ms[2] = {0, 0};  // relay variants' modelled time (keep-local, fuse-local)
   // Algorithmic bytes per run for THIS rank:
   int64_t hbm_read = 0;      // bytes of terms read from this GPU's HBM
   int64_t hbm_write = 0;     // bytes written to this GPU's HBM
@@ -150,7 +151,9 @@ class Program {
   };
 
   void lower(const CommPlan* comm, const SwitchPlan* sw);
-  std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, bool relay);
+  enum class RelayMode { None, KeepLocal, FuseLocal };
+  std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, RelayMode mode);
+  double estimate_seconds(const std::vector<BoxTask>& tasks, int phases);
   void choose_replicas(std::vector<BoxTask>& tasks);
   std::vector<BoxTask> spread_shared(std::vector<BoxTask> tasks);
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
@@ -173,6 +176,7 @@ class Program {
   std::vector<DevicePhase> dphases_;
   void* dev_block_ = nullptr;
   bool profiling_ = false;
+  bool remote_final_writes_ = false;  // last phase stores into peers' shards
   std::vector<cudaEvent_t> events_;  // 2 per phase per profiled run
   size_t events_used_ = 0;
   ProgramStats stats_;
