@@ -350,8 +350,9 @@ def main():
                     "dominant": {"phase": dom, "hbm_frac": (rd + wr) / (sph[dom] * 1e-3) / 1e9 / peak,
                                  "nvlink_gbs": nv / (sph[dom] * 1e-3) / 1e9},
                     "program": {k: sst[k] for k in ("phases", "plan_phases", "tasks", "items", "fused_tasks",
-                                                    "relay_outputs", "tma_items", "hbm_read", "hbm_write",
-                                                    "nvlink_in", "nvlink_out", "kernels_per_run")},
+                                                    "relay_outputs", "replica_swaps", "shared_chunks",
+                                                    "pushed_copies", "model_ms", "tma_items", "hbm_read",
+                                                    "hbm_write", "nvlink_in", "nvlink_out", "kernels_per_run")},
                     "flags": args.flags}
             if world > 1:
                 import torch.distributed as dist

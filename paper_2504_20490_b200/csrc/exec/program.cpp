@@ -293,6 +293,18 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   auto finish = [&](std::vector<BoxTask> ts) {
     if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) ts = spread_shared(std::move(ts));
     if (!(flags_ & HS_PROG_NO_MERGE)) ts = merge_outputs(std::move(ts));
+    // Single-output copies run on the rank holding the input (push: posted
+    // NVLink stores instead of round-trip reads); a copy with several outputs
+    // stays a pull -- one read, many local writes.
+    if (ctx_.world() > 1 && !(flags_ & HS_PROG_PULL_COPIES))
+      for (BoxTask& t : ts)
+        if (t.terms.size() == 1 && t.dsts.size() == 1) {
+          const int src = rank_of(t.terms[0], t.tensor);
+          if (src != t.rank) {
+            t.rank = src;
+            stats_.pushed_copies += 1;
+          }
+        }
     return ts;
   };
   if (two_phase && (ctx_.world() == 1 || (flags_ & HS_PROG_FUSE_PHASES))) {
@@ -314,7 +326,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     stats_ = stats0;
     std::vector<BoxTask> b = finish(fuse_phases(std::move(tasks), RelayMode::FuseLocal));
     const double ca = estimate_seconds(a, phases_a), cb = estimate_seconds(b, n_phases_);
-    if (ca <= cb) {
+    if (ca <= 0.85 * cb) {  // the model is coarse: keep-local must win clearly
       tasks = std::move(a);
       n_phases_ = phases_a;
       stats_ = stats_a;
@@ -691,8 +703,7 @@ double Program::estimate_seconds(const std::vector<BoxTask>& tasks, int phases) 
 // per rank along the box's outermost splittable dim; each rank computes its
 // chunk once and stores it to every output (local or over NVLink).  A
 // reduce-scatter + all-gather, with the inputs of each chunk read once.
-// Then single-input copies run on the rank that holds the input (push:
-// posted NVLink stores instead of round-trip reads).
+// Applied only where it lowers the busiest rank's NVLink bytes.
 std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
   std::map<std::string, std::vector<int>> same;
@@ -724,7 +735,41 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
     int split = -1;
     for (size_t d = 0; d < T.box.bounds.size() && split < 0; ++d)
       if (T.box.bounds[d][1] - T.box.bounds[d][0] >= static_cast<int64_t>(ranks.size())) split = static_cast<int>(d);
-    if (ranks.size() < 2 || dsts.size() > static_cast<size_t>(kMaxOuts) || T.terms.empty() || split < 0) {
+    // NVLink bytes per rank (in, out) with and without sharing, in box units:
+    // unshared, each rank pulls every remote input once for all its outputs;
+    // shared, each rank pulls 1/R of the remote inputs and stores its chunk
+    // into every output on another rank.
+    bool worth = false;
+    if (ranks.size() >= 2 && split >= 0) {
+      const int W = ctx_.world();
+      const double R = static_cast<double>(ranks.size());
+      std::vector<double> in0(W, 0), out0(W, 0), in1(W, 0), out1(W, 0);
+      std::vector<int> term_rank;
+      for (const Operand& o : T.terms) term_rank.push_back(rank_of(o, T.tensor));
+      for (int r : ranks)
+        for (int tr : term_rank)
+          if (tr != r) {
+            in0[r] += 1;
+            out0[tr] += 1;
+            in1[r] += 1 / R;
+            out1[tr] += 1 / R;
+          }
+      for (int r : ranks)
+        for (const Operand& o : dsts) {
+          const int orank = rank_of(o, T.tensor);
+          if (orank != r) {
+            out1[r] += 1 / R;
+            in1[orank] += 1 / R;
+          }
+        }
+      double m0 = 0, m1 = 0;
+      for (int r = 0; r < W; ++r) {
+        m0 = std::max({m0, in0[r], out0[r]});
+        m1 = std::max({m1, in1[r], out1[r]});
+      }
+      worth = m1 < 0.9 * m0;
+    }
+    if (!worth || dsts.size() > static_cast<size_t>(kMaxOuts) || T.terms.empty()) {
       for (int i : idx) out.push_back(tasks[i]);
       continue;
     }
@@ -741,15 +786,6 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
       out.push_back(std::move(chunk));
     }
   }
-  if (!(flags_ & HS_PROG_PULL_COPIES))
-    for (BoxTask& t : out)
-      if (t.terms.size() == 1) {
-        const int src = rank_of(t.terms[0], t.tensor);
-        if (src != t.rank) {
-          t.rank = src;
-          stats_.pushed_copies += 1;
-        }
-      }
   return out;
 }
 
