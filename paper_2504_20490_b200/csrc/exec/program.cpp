@@ -290,22 +290,50 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
-  auto finish = [&](std::vector<BoxTask> ts) {
-    if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) ts = spread_shared(std::move(ts));
-    if (!(flags_ & HS_PROG_NO_MERGE)) ts = merge_outputs(std::move(ts));
-    // Single-output copies run on the rank holding the input (push: posted
-    // NVLink stores instead of round-trip reads); a copy with several outputs
-    // stays a pull -- one read, many local writes.
-    if (ctx_.world() > 1 && !(flags_ & HS_PROG_PULL_COPIES))
-      for (BoxTask& t : ts)
-        if (t.terms.size() == 1 && t.dsts.size() == 1) {
-          const int src = rank_of(t.terms[0], t.tensor);
-          if (src != t.rank) {
-            t.rank = src;
-            stats_.pushed_copies += 1;
-          }
+  // Cross-rank rewrites (world > 1): sharing identical tasks across ranks
+  // and pushing single-output copies are each a win on some plans and a loss
+  // on others (they move HBM and link work between ranks), so every
+  // combination allowed by the flags is built and the one with the lowest
+  // modelled time (per-rank HBM / NVLink-in / NVLink-out bytes) is kept.
+  auto push_copies = [&](std::vector<BoxTask>& ts) {
+    int64_t n = 0;
+    for (BoxTask& t : ts)
+      if (t.terms.size() == 1 && t.dsts.size() == 1) {
+        const int src = rank_of(t.terms[0], t.tensor);
+        if (src != t.rank) {
+          t.rank = src;
+          ++n;
         }
-    return ts;
+      }
+    return n;
+  };
+  auto finish = [&](std::vector<BoxTask> ts) {
+    if (ctx_.world() == 1) return (flags_ & HS_PROG_NO_MERGE) ? ts : merge_outputs(std::move(ts));
+    std::vector<BoxTask> best;
+    double best_s = 0;
+    int64_t best_chunks = 0, best_pushed = 0;
+    for (int share = 0; share < 2; ++share) {
+      if (share && (flags_ & HS_PROG_NO_SHARE)) continue;
+      for (int push = 0; push < 2; ++push) {
+        if (push && (flags_ & HS_PROG_PULL_COPIES)) continue;
+        const int64_t chunks0 = stats_.shared_chunks;
+        std::vector<BoxTask> v = share ? spread_shared(ts) : ts;
+        const int64_t chunks = stats_.shared_chunks - chunks0;
+        stats_.shared_chunks = chunks0;
+        if (!(flags_ & HS_PROG_NO_MERGE)) v = merge_outputs(std::move(v));
+        const int64_t pushed = push ? push_copies(v) : 0;
+        const double sec = estimate_seconds(v, n_phases_);
+        if (best.empty() || sec < best_s * 0.98) {
+          best = std::move(v);
+          best_s = sec;
+          best_chunks = chunks;
+          best_pushed = pushed;
+        }
+      }
+    }
+    stats_.shared_chunks += best_chunks;
+    stats_.pushed_copies += best_pushed;
+    return best;
   };
   if (two_phase && (ctx_.world() == 1 || (flags_ & HS_PROG_FUSE_PHASES))) {
     // world 1: fuse everything fusable (HS_PROG_FUSE_PHASES forces it at
@@ -735,39 +763,43 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
     int split = -1;
     for (size_t d = 0; d < T.box.bounds.size() && split < 0; ++d)
       if (T.box.bounds[d][1] - T.box.bounds[d][0] >= static_cast<int64_t>(ranks.size())) split = static_cast<int>(d);
-    // NVLink bytes per rank (in, out) with and without sharing, in box units:
-    // unshared, each rank pulls every remote input once for all its outputs;
-    // shared, each rank pulls 1/R of the remote inputs and stores its chunk
-    // into every output on another rank.
+    // Per-rank time with and without sharing, in box units (HBM counted at
+    // 1/9 of a link byte: 6.3 TB/s vs 0.7 TB/s): unshared, every rank reads
+    // each input once for all its outputs; shared, each rank reads 1/R of the
+    // inputs and stores its chunk into every output on another rank.
     bool worth = false;
     if (ranks.size() >= 2 && split >= 0) {
       const int W = ctx_.world();
       const double R = static_cast<double>(ranks.size());
-      std::vector<double> in0(W, 0), out0(W, 0), in1(W, 0), out1(W, 0);
-      std::vector<int> term_rank;
-      for (const Operand& o : T.terms) term_rank.push_back(rank_of(o, T.tensor));
+      std::vector<double> h0(W, 0), in0(W, 0), out0(W, 0), h1(W, 0), in1(W, 0), out1(W, 0);
       for (int r : ranks)
-        for (int tr : term_rank)
+        for (const Operand& o : T.terms) {
+          const int tr = rank_of(o, T.tensor);
+          h0[tr] += 1;
+          h1[tr] += 1 / R;
           if (tr != r) {
             in0[r] += 1;
             out0[tr] += 1;
             in1[r] += 1 / R;
             out1[tr] += 1 / R;
           }
-      for (int r : ranks)
-        for (const Operand& o : dsts) {
-          const int orank = rank_of(o, T.tensor);
+        }
+      for (const Operand& o : dsts) {
+        const int orank = rank_of(o, T.tensor);
+        h0[orank] += 1;
+        h1[orank] += 1;
+        for (int r : ranks)
           if (orank != r) {
             out1[r] += 1 / R;
             in1[orank] += 1 / R;
           }
-        }
+      }
       double m0 = 0, m1 = 0;
       for (int r = 0; r < W; ++r) {
-        m0 = std::max({m0, in0[r], out0[r]});
-        m1 = std::max({m1, in1[r], out1[r]});
+        m0 = std::max({m0, h0[r] / 9, in0[r], out0[r]});
+        m1 = std::max({m1, h1[r] / 9, in1[r], out1[r]});
       }
-      worth = m1 < 0.9 * m0;
+      worth = m1 < 0.95 * m0;
     }
     if (!worth || dsts.size() > static_cast<size_t>(kMaxOuts) || T.terms.empty()) {
       for (int i : idx) out.push_back(tasks[i]);
