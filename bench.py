@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--sweep", default=None,
                     help="comma list of workloads (or 'all'): one JSON line per workload instead "
                          "of the headline line")
+    ap.add_argument("--no-tune", action="store_true", help="world > 1: no autotuning of the program variant")
     ap.add_argument("--flags", type=int, default=0,
                     help="HS_PROG_* bits: 1 fuse, 2 no-fuse, 4 no-TMA, 8 no-merge (14 = plain baseline)")
     return ap.parse_args()
@@ -261,7 +262,7 @@ def main():
     import numpy as np
     import torch
     from paper_2504_20490_b200 import hshard as H
-    from paper_2504_20490_b200.executor import Context, Program, ShardLayout
+    from paper_2504_20490_b200.executor import Context, Program, ShardLayout, autotune
 
     torch.cuda.set_device(local)
     free, _ = torch.cuda.mem_get_info(local)
@@ -288,11 +289,23 @@ def main():
         else:
             plan = H.plan_switch(work.transitions, work.dtype)
         lay = ShardLayout(ctx, plan, work.n_virtual)
-        prog = Program(ctx, plan, lay, args.flags)
+        if world > 1 and args.flags == 0 and not args.no_tune:
+            # cross-rank rewrite variants are chosen by timing them (untimed warm-up)
+            lay.fill_src(1, "grid", sp)
+            stream.synchronize()
+            prog, tuned = autotune(ctx, plan, lay, stream=stream,
+                                   steps=3 if W.resident_bytes(work) > 20e9 else 10)
+            tune_log[work.name] = {"chosen_flags": prog_flags(prog, tuned), "ms_by_flags": tuned}
+        else:
+            prog = Program(ctx, plan, lay, args.flags)
         return plan, lay, prog
 
     stream = torch.cuda.Stream(device=local)
     sp = stream.cuda_stream
+    tune_log = {}
+
+    def prog_flags(prog, tuned):
+        return min(tuned, key=tuned.get) if tuned else args.flags
 
     def timed(prog, steps, warmup, profile=False):
         for _ in range(warmup):
@@ -353,7 +366,7 @@ def main():
                                                     "relay_outputs", "replica_swaps", "shared_chunks",
                                                     "pushed_copies", "model_ms", "tma_items", "hbm_read",
                                                     "hbm_write", "nvlink_in", "nvlink_out", "kernels_per_run")},
-                    "flags": args.flags}
+                    "flags": args.flags, "tuning": tune_log.get(name)}
             if world > 1:
                 import torch.distributed as dist
                 per = [None] * world
@@ -480,7 +493,7 @@ def main():
                        "plan": [s["kind"] for s in plan.json()["bottom"] + plan.json()["top"]]
                        if w.kind == "classify" else "fused Bsr",
                        "dst_resident_bytes": total_dst, "l2": "inputs larger than L2 (no flush)",
-                       "program_flags": args.flags,
+                       "program_flags": args.flags, "tuning": tune_log.get(w.name),
                        "program": {k: st[k] for k in ("phases", "plan_phases", "tasks", "items",
                                                       "fused_tasks", "tma_items", "hbm_read",
                                                       "hbm_write", "nvlink_in", "nvlink_out")}},

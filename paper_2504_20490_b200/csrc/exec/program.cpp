@@ -290,79 +290,36 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
-  // Cross-rank rewrites (world > 1): sharing identical tasks across ranks
-  // and pushing single-output copies are each a win on some plans and a loss
-  // on others (they move HBM and link work between ranks), so every
-  // combination allowed by the flags is built and the one with the lowest
-  // modelled time (per-rank HBM / NVLink-in / NVLink-out bytes) is kept.
-  auto push_copies = [&](std::vector<BoxTask>& ts) {
-    int64_t n = 0;
-    for (BoxTask& t : ts)
-      if (t.terms.size() == 1 && t.dsts.size() == 1) {
-        const int src = rank_of(t.terms[0], t.tensor);
-        if (src != t.rank) {
-          t.rank = src;
-          ++n;
-        }
-      }
-    return n;
-  };
+  // Cross-rank rewrites (world > 1), each behind a flag because which wins
+  // depends on the plan's balance (executor.autotune() times the variants):
+  //   share -- identical tasks on several ranks become per-rank chunks;
+  //   push  -- single-output copies run on the rank holding the input.
   auto finish = [&](std::vector<BoxTask> ts) {
-    if (ctx_.world() == 1) return (flags_ & HS_PROG_NO_MERGE) ? ts : merge_outputs(std::move(ts));
-    std::vector<BoxTask> best;
-    double best_s = 0;
-    int64_t best_chunks = 0, best_pushed = 0;
-    for (int share = 0; share < 2; ++share) {
-      if (share && (flags_ & HS_PROG_NO_SHARE)) continue;
-      for (int push = 0; push < 2; ++push) {
-        if (push && (flags_ & HS_PROG_PULL_COPIES)) continue;
-        const int64_t chunks0 = stats_.shared_chunks;
-        std::vector<BoxTask> v = share ? spread_shared(ts) : ts;
-        const int64_t chunks = stats_.shared_chunks - chunks0;
-        stats_.shared_chunks = chunks0;
-        if (!(flags_ & HS_PROG_NO_MERGE)) v = merge_outputs(std::move(v));
-        const int64_t pushed = push ? push_copies(v) : 0;
-        const double sec = estimate_seconds(v, n_phases_);
-        if (best.empty() || sec < best_s * 0.98) {
-          best = std::move(v);
-          best_s = sec;
-          best_chunks = chunks;
-          best_pushed = pushed;
+    if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) ts = spread_shared(std::move(ts));
+    if (!(flags_ & HS_PROG_NO_MERGE)) ts = merge_outputs(std::move(ts));
+    if (ctx_.world() > 1 && !(flags_ & HS_PROG_PULL_COPIES))
+      for (BoxTask& t : ts)
+        if (t.terms.size() == 1 && t.dsts.size() == 1) {
+          const int src = rank_of(t.terms[0], t.tensor);
+          if (src != t.rank) {
+            t.rank = src;
+            stats_.pushed_copies += 1;
+          }
         }
-      }
-    }
-    stats_.shared_chunks += best_chunks;
-    stats_.pushed_copies += best_pushed;
-    return best;
+    return ts;
   };
   if (two_phase && (ctx_.world() == 1 || (flags_ & HS_PROG_FUSE_PHASES))) {
     // world 1: fuse everything fusable (HS_PROG_FUSE_PHASES forces it at
     // world > 1, pulling raw inputs over NVLink)
     tasks = finish(fuse_phases(std::move(tasks), RelayMode::None));
   } else if (two_phase && !(flags_ & HS_PROG_NO_RELAY)) {
-    // world > 1: relays for remote mid reads.  Whether a task that waits for
-    // a relay should also fuse its local groups (less HBM traffic, but done
-    // after the barrier) or keep them in phase 1 (concurrent with the remote
-    // producers) depends on the plan: build both, keep the cheaper by the
-    // per-rank HBM / NVLink byte model.
-    const int phases0 = n_phases_;
-    const ProgramStats stats0 = stats_;
-    std::vector<BoxTask> a = finish(fuse_phases(tasks, RelayMode::KeepLocal));
-    const int phases_a = n_phases_;
-    const ProgramStats stats_a = stats_;
-    n_phases_ = phases0;
-    stats_ = stats0;
-    std::vector<BoxTask> b = finish(fuse_phases(std::move(tasks), RelayMode::FuseLocal));
-    const double ca = estimate_seconds(a, phases_a), cb = estimate_seconds(b, n_phases_);
-    if (ca <= 0.85 * cb) {  // the model is coarse: keep-local must win clearly
-      tasks = std::move(a);
-      n_phases_ = phases_a;
-      stats_ = stats_a;
-    } else {
-      tasks = std::move(b);
-    }
-    stats_.model_ms[0] = ca * 1e3;
-    stats_.model_ms[1] = cb * 1e3;
+    // world > 1: relays for remote mid reads.  A task that waits for a relay
+    // fuses its local groups too (least HBM traffic) unless
+    // HS_PROG_RELAY_KEEP_LOCAL asks to compute them before the barrier,
+    // concurrently with the remote producers.
+    const RelayMode mode = (flags_ & HS_PROG_RELAY_KEEP_LOCAL) ? RelayMode::KeepLocal : RelayMode::FuseLocal;
+    tasks = finish(fuse_phases(std::move(tasks), mode));
+    stats_.model_ms[0] = estimate_seconds(tasks, n_phases_) * 1e3;
   } else {
     tasks = finish(std::move(tasks));
   }
@@ -731,9 +688,7 @@ double Program::estimate_seconds(const std::vector<BoxTask>& tasks, int phases) 
 // per rank along the box's outermost splittable dim; each rank computes its
 // chunk once and stores it to every output (local or over NVLink).  A
 // reduce-scatter + all-gather, with the inputs of each chunk read once.
-// Applied only where it lowers the busiest rank's NVLink bytes.
 std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
-  auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
   std::map<std::string, std::vector<int>> same;
   std::vector<std::string> order;
   for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
@@ -763,44 +718,7 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
     int split = -1;
     for (size_t d = 0; d < T.box.bounds.size() && split < 0; ++d)
       if (T.box.bounds[d][1] - T.box.bounds[d][0] >= static_cast<int64_t>(ranks.size())) split = static_cast<int>(d);
-    // Per-rank time with and without sharing, in box units (HBM counted at
-    // 1/9 of a link byte: 6.3 TB/s vs 0.7 TB/s): unshared, every rank reads
-    // each input once for all its outputs; shared, each rank reads 1/R of the
-    // inputs and stores its chunk into every output on another rank.
-    bool worth = false;
-    if (ranks.size() >= 2 && split >= 0) {
-      const int W = ctx_.world();
-      const double R = static_cast<double>(ranks.size());
-      std::vector<double> h0(W, 0), in0(W, 0), out0(W, 0), h1(W, 0), in1(W, 0), out1(W, 0);
-      for (int r : ranks)
-        for (const Operand& o : T.terms) {
-          const int tr = rank_of(o, T.tensor);
-          h0[tr] += 1;
-          h1[tr] += 1 / R;
-          if (tr != r) {
-            in0[r] += 1;
-            out0[tr] += 1;
-            in1[r] += 1 / R;
-            out1[tr] += 1 / R;
-          }
-        }
-      for (const Operand& o : dsts) {
-        const int orank = rank_of(o, T.tensor);
-        h0[orank] += 1;
-        h1[orank] += 1;
-        for (int r : ranks)
-          if (orank != r) {
-            out1[r] += 1 / R;
-            in1[orank] += 1 / R;
-          }
-      }
-      double m0 = 0, m1 = 0;
-      for (int r = 0; r < W; ++r) {
-        m0 = std::max({m0, h0[r] / 9, in0[r], out0[r]});
-        m1 = std::max({m1, h1[r] / 9, in1[r], out1[r]});
-      }
-      worth = m1 < 0.95 * m0;
-    }
+    const bool worth = ranks.size() >= 2 && split >= 0;
     if (!worth || dsts.size() > static_cast<size_t>(kMaxOuts) || T.terms.empty()) {
       for (int i : idx) out.push_back(tasks[i]);
       continue;

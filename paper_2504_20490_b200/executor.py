@@ -34,6 +34,7 @@ HS_PROG_NO_RELAY = 32      # world > 1: pull remote mid boxes instead of relay s
 HS_PROG_NO_REPLICA = 64    # world > 1: no replica-aware source choice
 HS_PROG_NO_SHARE = 128     # world > 1: no cross-rank chunking of identical tasks
 HS_PROG_PULL_COPIES = 256  # world > 1: copies pull (run on the destination's rank)
+HS_PROG_RELAY_KEEP_LOCAL = 512  # world > 1: relay-waiting tasks keep local groups before the barrier
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -273,3 +274,55 @@ class Program:
 
     def __del__(self):
         self.close()
+
+
+AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES,
+                       HS_PROG_RELAY_KEEP_LOCAL]
+
+
+def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps: int = 5,
+             candidates=None, group=None):
+    """Pick the program variant (HS_PROG_* flags of the cross-rank rewrites) that runs fastest.
+
+    Every candidate is compiled and timed for `steps` runs with CUDA events on `stream`; the
+    max over ranks decides (all ranks take the same choice).  Results are bit-identical across
+    variants -- only the placement of work between ranks differs.  world == 1 has nothing to
+    tune.  Returns (program, {flags: ms}).
+    """
+    if ctx.world == 1:
+        return Program(ctx, plan, layout, 0), {}
+    import torch
+    import torch.distributed as dist
+    cands = list(candidates if candidates is not None else AUTOTUNE_CANDIDATES)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    sp = s.cuda_stream
+    best, best_ms, timings = None, None, {}
+    for flags in cands:
+        prog = Program(ctx, plan, layout, flags)
+        if flags & HS_PROG_RELAY_KEEP_LOCAL and prog.stats()["plan_phases"] < 2:
+            prog.close()
+            continue
+        for _ in range(2):
+            prog.run(sp)
+        s.synchronize()
+        ctx.sync()
+        dist.barrier(group=group)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            a.record()
+            for _ in range(steps):
+                prog.run(sp)
+            b.record()
+        b.synchronize()
+        ctx.sync()
+        t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        ms = float(t.item())
+        timings[flags] = ms
+        if best is None or ms < best_ms:
+            if best is not None:
+                best.close()
+            best, best_ms = prog, ms
+        else:
+            prog.close()
+    return best, timings
