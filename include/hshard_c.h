@@ -114,7 +114,8 @@ enum {
   HS_PROG_NO_REPLICA = 64,  /* world > 1: read every term from the device the plan names */
   HS_PROG_NO_SHARE = 128,   /* world > 1: identical tasks on several ranks are not chunked */
   HS_PROG_PULL_COPIES = 256, /* world > 1: copies run on the destination's rank (pull) */
-  HS_PROG_RELAY_KEEP_LOCAL = 512 /* world > 1: relay-waiting tasks keep local groups in phase 1 */
+  HS_PROG_RELAY_KEEP_LOCAL = 512, /* world > 1: relay-waiting tasks keep local groups in phase 1 */
+  HS_PROG_PUSH_ALL = 1024         /* world > 1: every copy runs on its input's rank */
 };
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);

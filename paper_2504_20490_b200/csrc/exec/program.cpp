@@ -294,8 +294,19 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   // depends on the plan's balance (executor.autotune() times the variants):
   //   share -- identical tasks on several ranks become per-rank chunks;
   //   push  -- single-output copies run on the rank holding the input.
+  //   push-all -- every copy runs on the input's rank, even one that stores
+  //               to several outputs (moves work off busy receivers).
   auto finish = [&](std::vector<BoxTask> ts) {
     if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) ts = spread_shared(std::move(ts));
+    if (ctx_.world() > 1 && (flags_ & HS_PROG_PUSH_ALL))
+      for (BoxTask& t : ts)
+        if (t.terms.size() == 1) {
+          const int src = rank_of(t.terms[0], t.tensor);
+          if (src != t.rank) {
+            t.rank = src;
+            stats_.pushed_copies += 1;
+          }
+        }
     if (!(flags_ & HS_PROG_NO_MERGE)) ts = merge_outputs(std::move(ts));
     if (ctx_.world() > 1 && !(flags_ & HS_PROG_PULL_COPIES))
       for (BoxTask& t : ts)

@@ -35,6 +35,7 @@ HS_PROG_NO_REPLICA = 64    # world > 1: no replica-aware source choice
 HS_PROG_NO_SHARE = 128     # world > 1: no cross-rank chunking of identical tasks
 HS_PROG_PULL_COPIES = 256  # world > 1: copies pull (run on the destination's rank)
 HS_PROG_RELAY_KEEP_LOCAL = 512  # world > 1: relay-waiting tasks keep local groups before the barrier
+HS_PROG_PUSH_ALL = 1024    # world > 1: every copy runs on its input's rank (before output merging)
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -277,7 +278,7 @@ class Program:
 
 
 AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES,
-                       HS_PROG_RELAY_KEEP_LOCAL]
+                       HS_PROG_PUSH_ALL, HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE, HS_PROG_RELAY_KEEP_LOCAL]
 
 
 def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps: int = 5,
