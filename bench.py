@@ -268,6 +268,8 @@ def main():
     free, _ = torch.cuda.mem_get_info(local)
     arena = max(8 << 30, free - (10 << 30))
     ctx = Context(arena, rank=rank, world=world, gpu=local)
+    if world > 1 and args.flags & 2048:
+        ctx.init_nccl()
 
     def allreduce_max(x: float) -> float:
         if world == 1:

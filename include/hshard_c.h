@@ -94,6 +94,11 @@ int hs_ctx_ipc_handle(hs_ctx* ctx, unsigned char* out128);
  * world x 128 bytes).  Enables peer access.  Call once, after create. */
 int hs_ctx_open_peers(hs_ctx* ctx, const unsigned char* all_handles);
 
+/* NCCL communicator over the same ranks, for the HS_PROG_NCCL baseline
+ * transport: rank 0 creates the id, the host broadcasts it, every rank inits. */
+int hs_nccl_unique_id(unsigned char* out128);
+int hs_ctx_nccl_init(hs_ctx* ctx, const unsigned char* id128);
+
 /* Bump allocator inside the arena: offsets are identical on every rank when
  * every rank performs the same sequence of allocations (symmetric heap). */
 int hs_ctx_alloc(hs_ctx* ctx, size_t bytes, size_t* offset);
@@ -115,7 +120,10 @@ enum {
   HS_PROG_NO_SHARE = 128,   /* world > 1: identical tasks on several ranks are not chunked */
   HS_PROG_PULL_COPIES = 256, /* world > 1: copies run on the destination's rank (pull) */
   HS_PROG_RELAY_KEEP_LOCAL = 512, /* world > 1: relay-waiting tasks keep local groups in phase 1 */
-  HS_PROG_PUSH_ALL = 1024         /* world > 1: every copy runs on its input's rank */
+  HS_PROG_PUSH_ALL = 1024,        /* world > 1: every copy runs on its input's rank */
+  HS_PROG_NCCL = 2048             /* world > 1: baseline transport -- remote inputs are packed,
+                                     exchanged with grouped ncclSend/ncclRecv, and read locally
+                                     (no peer-memory access, no device barriers) */
 };
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);

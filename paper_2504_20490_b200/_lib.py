@@ -64,6 +64,8 @@ def _load() -> ctypes.CDLL:
         "hs_ctx_ipc_handle": (c_int, [c_void_p, c_char_p]),
         "hs_ctx_open_peers": (c_int, [c_void_p, c_char_p]),
         "hs_ctx_alloc": (c_int, [c_void_p, c_size_t, P(c_size_t)]),
+        "hs_nccl_unique_id": (c_int, [c_char_p]),
+        "hs_ctx_nccl_init": (c_int, [c_void_p, c_char_p]),
         "hs_ctx_reset_alloc": (c_int, [c_void_p, c_size_t]),
         "hs_prog_compile": (c_int, [c_void_p, c_void_p, P(c_int), c_int, P(c_size_t), P(c_size_t),
                                     c_int, P(c_void_p)]),

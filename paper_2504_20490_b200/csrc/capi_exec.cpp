@@ -2,6 +2,8 @@
 #include <cstring>
 #include <memory>
 
+#include <nccl.h>
+
 #include "capi_common.hpp"
 #include "exec/program.hpp"
 
@@ -72,6 +74,19 @@ int hs_ctx_ipc_handle(hs_ctx* ctx, unsigned char* out128) {
 
 int hs_ctx_open_peers(hs_ctx* ctx, const unsigned char* all) {
   return guarded([&] { ctx->c->open_peers(all); });
+}
+
+int hs_nccl_unique_id(unsigned char* out128) {
+  return guarded([&] {
+    ncclUniqueId uid;
+    const ncclResult_t r = ncclGetUniqueId(&uid);
+    if (r != ncclSuccess) fail(Errc::CommError, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out128, &uid, sizeof(uid));
+  });
+}
+
+int hs_ctx_nccl_init(hs_ctx* ctx, const unsigned char* id128) {
+  return guarded([&] { ctx->c->nccl_init(id128); });
 }
 
 int hs_ctx_alloc(hs_ctx* ctx, size_t bytes, size_t* offset) {

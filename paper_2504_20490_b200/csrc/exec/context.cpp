@@ -8,6 +8,8 @@
 #include <cstring>
 #include <string>
 
+#include <nccl.h>
+
 #include "program.hpp"
 
 namespace hshard::exec {
@@ -43,6 +45,7 @@ Context::Context(int rank, int world, int gpu, size_t arena_bytes)
 Context::~Context() {
   cudaSetDevice(gpu_);
   cudaDeviceSynchronize();
+  if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (int r = 0; r < world_; ++r) {
     if (r == rank_) continue;
     if (peer_arena_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
@@ -114,6 +117,18 @@ void Context::barrier(cudaStream_t s) {
   cuda_check(launch_barrier(d_peer_flags_, world_, rank_, epoch_, 20ull * 1000 * 1000 * 1000,
                             barrier_error_, s),
              "barrier launch");
+}
+
+void Context::nccl_init(const unsigned char id[128]) {
+  if (nccl_comm_) return;
+  ncclUniqueId uid;
+  static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(&uid, id, sizeof(uid));
+  cuda_check(cudaSetDevice(gpu_), "cudaSetDevice");
+  ncclComm_t comm;
+  const ncclResult_t r = ncclCommInitRank(&comm, world_, uid, rank_);
+  if (r != ncclSuccess) fail(Errc::CommError, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  nccl_comm_ = comm;
 }
 
 void Context::check_barrier_error() {

@@ -26,6 +26,8 @@
 #include <set>
 #include <sstream>
 
+#include <nccl.h>
+
 #include "hshard_c.h"
 #include "planner_internal.hpp"
 #include "program.hpp"
@@ -287,6 +289,14 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   stats_.plan_phases = n_phases_;
 
   // ---- rewrites (results are bit-identical by construction; see header)
+  nccl_mode_ = ctx_.world() > 1 && (flags_ & HS_PROG_NCCL);
+  if (nccl_mode_) {
+    // baseline transport: plain pulls, no peer stores (the rewrites below
+    // that store into peers are off); remote inputs are staged in stage_for_nccl()
+    if (!ctx_.nccl_comm()) fail(Errc::CommError, "HS_PROG_NCCL needs hs_ctx_nccl_init first");
+    flags_ |= HS_PROG_NO_RELAY | HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES;
+    flags_ &= ~(HS_PROG_PUSH_ALL | HS_PROG_FUSE_PHASES);
+  }
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
@@ -335,6 +345,8 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     tasks = finish(std::move(tasks));
   }
 
+  if (nccl_mode_) stage_for_nccl(tasks);
+
   // Symmetric placement of the intermediate (mid) and relay shards still in
   // use: every rank packs its own densely from one common base.
   if (mid_state_ >= 0) {
@@ -342,7 +354,9 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     for (const BoxTask& t : tasks)
       for (const auto* ops : {&t.dsts, &t.terms})
         for (const Operand& o : *ops)
-          if (o.state >= mid_state_ && o.state != static_cast<int>(final_state_)) used_keys.insert({o.state, o.dev});
+          if (o.state >= mid_state_ && o.state != static_cast<int>(final_state_) &&
+              o.state < staging_state_)
+            used_keys.insert({o.state, o.dev});
     if (!used_keys.empty()) {
       std::vector<size_t> used(ctx_.world(), 0);
       for (const auto& [st, dev] : used_keys) {
@@ -649,6 +663,94 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
     n_phases_ = 1;
   }
   return result;
+}
+
+// ---------------------------------------------------------------- NCCL baseline
+// HS_PROG_NCCL: every remote input of every task is first copied (a local
+// "pack" task on the owner) into a per-(phase, sender, receiver) message,
+// the messages of a phase go out as one ncclGroupStart / ncclSend x peers /
+// ncclRecv x peers / ncclGroupEnd, and the task reads its input from the
+// receive buffer.  Plan phase p becomes launched phases 2p (pack) and 2p+1
+// (compute).  This is the NCCL-carried executor the peer-memory kernels are
+// measured against.
+void Program::stage_for_nccl(std::vector<BoxTask>& tasks) {
+  const int W = ctx_.world();
+  const int P = n_phases_;
+  staging_state_ = static_cast<int>(states_.size());
+  const int send_state = staging_state_, recv_state = staging_state_ + 1;
+  states_.emplace_back();
+  states_.emplace_back();
+  struct Chunk {
+    int phase, src, dst, tensor;
+    size_t off;
+    DeviceId id;
+  };
+  std::vector<Chunk> chunks;
+  std::vector<std::map<std::pair<int, int>, size_t>> msg(P);  // (src, dst) -> bytes
+  std::vector<BoxTask> packs;
+  DeviceId next = 0;
+  for (BoxTask& t : tasks) {
+    for (Operand& o : t.terms) {
+      const ShardLoc& L = loc(o.state, t.tensor, o.dev);
+      if (L.rank == t.rank) continue;
+      size_t& u = msg[t.phase][{L.rank, t.rank}];
+      u = (u + 255) & ~size_t{255};
+      const size_t off = u;
+      u += static_cast<size_t>(t.box.cells()) * es_;
+      const DeviceId id = next++;
+      ShardLoc S;
+      S.region = t.box;
+      S.rank = L.rank;
+      states_[send_state][{t.tensor, id}] = S;
+      S.rank = t.rank;
+      states_[recv_state][{t.tensor, id}] = S;
+      BoxTask pack;
+      pack.phase = t.phase;
+      pack.kind = t.kind;
+      pack.tensor = t.tensor;
+      pack.box = t.box;
+      pack.rank = L.rank;
+      pack.dsts = {Operand{send_state, id}};
+      pack.terms = {o};
+      packs.push_back(std::move(pack));
+      chunks.push_back({t.phase, L.rank, t.rank, t.tensor, off, id});
+      o = Operand{recv_state, id};
+    }
+  }
+  // Message layout: every rank's send area ordered by (phase, receiver), its
+  // receive area by (phase, sender); both sides agree on chunk offsets.
+  std::vector<std::map<std::pair<int, int>, size_t>> send_at(W), recv_at(W);
+  std::vector<size_t> send_total(W, 0), recv_total(W, 0);
+  for (int p = 0; p < P; ++p)
+    for (const auto& [pair, bytes] : msg[p]) {
+      send_at[pair.first][{p, pair.second}] = send_total[pair.first];
+      send_total[pair.first] += (bytes + 255) & ~size_t{255};
+      recv_at[pair.second][{p, pair.first}] = recv_total[pair.second];
+      recv_total[pair.second] += (bytes + 255) & ~size_t{255};
+    }
+  const size_t send_base = ctx_.alloc(*std::max_element(send_total.begin(), send_total.end()) + 256);
+  const size_t recv_base = ctx_.alloc(*std::max_element(recv_total.begin(), recv_total.end()) + 256);
+  for (const Chunk& c : chunks) {
+    states_[send_state][{c.tensor, c.id}].offset = send_base + send_at[c.src][{c.phase, c.dst}] + c.off;
+    states_[recv_state][{c.tensor, c.id}].offset = recv_base + recv_at[c.dst][{c.phase, c.src}] + c.off;
+  }
+  const int me = ctx_.rank();
+  exchanges_.assign(P, {});
+  for (int p = 0; p < P; ++p)
+    for (const auto& [pair, bytes] : msg[p]) {
+      if (pair.first == me) {
+        exchanges_[p].push_back({pair.second, true, send_base + send_at[me][{p, pair.second}], bytes});
+        stats_.nvlink_out += static_cast<int64_t>(bytes);
+      }
+      if (pair.second == me) {
+        exchanges_[p].push_back({pair.first, false, recv_base + recv_at[me][{p, pair.first}], bytes});
+        stats_.nvlink_in += static_cast<int64_t>(bytes);
+      }
+    }
+  for (BoxTask& t : tasks) t.phase = 2 * t.phase + 1;
+  for (BoxTask& t : packs) t.phase = 2 * t.phase;
+  tasks.insert(tasks.end(), std::make_move_iterator(packs.begin()), std::make_move_iterator(packs.end()));
+  n_phases_ = 2 * P;
 }
 
 // ---------------------------------------------------------------- cost model
@@ -1006,7 +1108,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }
-  const int barriers = ctx_.world() > 1 ? n_phases_ + (remote_final_writes_ ? 1 : 0) : 0;
+  const int barriers = ctx_.world() > 1 && !nccl_mode_ ? n_phases_ + (remote_final_writes_ ? 1 : 0) : 0;
   stats_.kernels_per_run = launches + barriers;
 }
 
@@ -1029,14 +1131,30 @@ void Program::run(cudaStream_t s) {
   // destinations are complete when its stream is (callers still sync all
   // ranks before modifying sources).
   for (int p = 0; p < n_phases_; ++p) {
-    ctx_.barrier(s);
+    if (!nccl_mode_) ctx_.barrier(s);
     if (profiling_) event();
     for (const Launch& l : dphases_[p].launches)
       cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s),
                  "box_phase launch");
+    if (nccl_mode_ && p % 2 == 0 && !exchanges_[p / 2].empty()) {
+      // the pack phase is followed by the phase's message exchange
+      ncclComm_t comm = static_cast<ncclComm_t>(ctx_.nccl_comm());
+      auto nccl = [](ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) fail(Errc::CommError, std::string(what) + ": " + ncclGetErrorString(r));
+      };
+      nccl(ncclGroupStart(), "ncclGroupStart");
+      for (const Exchange& x : exchanges_[p / 2]) {
+        char* ptr = ctx_.arena() + x.offset;
+        if (x.send)
+          nccl(ncclSend(ptr, x.bytes, ncclChar, x.peer, comm, s), "ncclSend");
+        else
+          nccl(ncclRecv(ptr, x.bytes, ncclChar, x.peer, comm, s), "ncclRecv");
+      }
+      nccl(ncclGroupEnd(), "ncclGroupEnd");
+    }
     if (profiling_) event();
   }
-  if (remote_final_writes_) ctx_.barrier(s);
+  if (remote_final_writes_ && !nccl_mode_) ctx_.barrier(s);
 }
 
 void Program::run_host(const void* const* src_host, void* const* dst_host) {

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "hshard/resolve.hpp"
+#include "hshard_c.h"
 #include "hshard/switch.hpp"
 #include "kernels.cuh"
 
@@ -48,6 +49,10 @@ class Context {
 
   unsigned long long* scratch_counter() const { return counter_; }
 
+  // NCCL communicator over the same ranks (HS_PROG_NCCL baseline transport).
+  void nccl_init(const unsigned char id[128]);
+  void* nccl_comm() const { return nccl_comm_; }
+
  private:
   int rank_, world_, gpu_;
   int sm_count_ = 148;
@@ -63,6 +68,7 @@ class Context {
   unsigned int epoch_ = 0;
   bool peers_open_ = false;
   cudaStream_t stream_ = nullptr;
+  void* nccl_comm_ = nullptr;  // ncclComm_t
 };
 
 // Where one tensor's shard for one virtual device lives in one layout state.
@@ -154,6 +160,7 @@ class Program {
   enum class RelayMode { None, KeepLocal, FuseLocal };
   std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, RelayMode mode);
   double estimate_seconds(const std::vector<BoxTask>& tasks, int phases);
+  void stage_for_nccl(std::vector<BoxTask>& tasks);
   void choose_replicas(std::vector<BoxTask>& tasks);
   std::vector<BoxTask> spread_shared(std::vector<BoxTask> tasks);
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
@@ -177,6 +184,16 @@ class Program {
   void* dev_block_ = nullptr;
   bool profiling_ = false;
   bool remote_final_writes_ = false;  // last phase stores into peers' shards
+  // HS_PROG_NCCL baseline: per plan phase, this rank's grouped send/recv list
+  struct Exchange {
+    int peer;
+    bool send;
+    size_t offset;  // arena offset of the message
+    size_t bytes;
+  };
+  bool nccl_mode_ = false;
+  int staging_state_ = 1 << 30;
+  std::vector<std::vector<Exchange>> exchanges_;
   std::vector<cudaEvent_t> events_;  // 2 per phase per profiled run
   size_t events_used_ = 0;
   ProgramStats stats_;

@@ -36,6 +36,7 @@ HS_PROG_NO_SHARE = 128     # world > 1: no cross-rank chunking of identical task
 HS_PROG_PULL_COPIES = 256  # world > 1: copies pull (run on the destination's rank)
 HS_PROG_RELAY_KEEP_LOCAL = 512  # world > 1: relay-waiting tasks keep local groups before the barrier
 HS_PROG_PUSH_ALL = 1024    # world > 1: every copy runs on its input's rank (before output merging)
+HS_PROG_NCCL = 2048         # world > 1: NCCL grouped send/recv transport (baseline)
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -74,6 +75,17 @@ class Context:
         dist.all_gather(gathered, t, group=group)
         blob = b"".join(bytes(g.numpy().tobytes()) for g in gathered)
         check(LIB.hs_ctx_open_peers(self._h, blob))
+
+    def init_nccl(self, group=None) -> None:
+        """NCCL communicator over the same ranks (only the HS_PROG_NCCL baseline uses it)."""
+        import torch.distributed as dist
+        uid = [None]
+        if self.rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            check(LIB.hs_nccl_unique_id(buf))
+            uid[0] = buf.raw
+        dist.broadcast_object_list(uid, src=0, group=group)
+        check(LIB.hs_ctx_nccl_init(self._h, uid[0]))
 
     @property
     def handle(self):

@@ -31,6 +31,8 @@ def main():
     torch.cuda.set_device(local)
     ctx = Context(8 << 30, rank=rank, world=world, gpu=local)
     flag_sets = [int(x) for x in os.environ.get("HS_MGPU_FLAGS", "0,14,1").split(",")]
+    if any(f & 2048 for f in flag_sets):
+        ctx.init_nccl()
     results, ok = [], True
 
     def run_case(name, plan, n_virtual, src_of, dtype, mode):

@@ -26,7 +26,7 @@ def _gpus():
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("flags", ["0,14,1", "16,17,32,48", "128,256,480", "512,1024,1152"])  # see HS_PROG_*
+@pytest.mark.parametrize("flags", ["0,14,1", "16,17,32,48", "128,256,480", "512,1024,1152", "2048,2062"])  # see HS_PROG_*
 def test_multi_gpu_parity(tmp_path, flags):
     n = min(_gpus(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
