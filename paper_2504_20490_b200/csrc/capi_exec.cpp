@@ -2,9 +2,8 @@
 #include <cstring>
 #include <memory>
 
-#include <nccl.h>
-
 #include "capi_common.hpp"
+#include "exec/nccl_dyn.hpp"
 #include "exec/program.hpp"
 
 using namespace hshard;
@@ -79,8 +78,7 @@ int hs_ctx_open_peers(hs_ctx* ctx, const unsigned char* all) {
 int hs_nccl_unique_id(unsigned char* out128) {
   return guarded([&] {
     ncclUniqueId uid;
-    const ncclResult_t r = ncclGetUniqueId(&uid);
-    if (r != ncclSuccess) fail(Errc::CommError, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    exec::nccl::check(exec::nccl::api().GetUniqueId(&uid), "ncclGetUniqueId");
     std::memcpy(out128, &uid, sizeof(uid));
   });
 }

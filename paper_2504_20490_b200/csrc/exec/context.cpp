@@ -8,8 +8,7 @@
 #include <cstring>
 #include <string>
 
-#include <nccl.h>
-
+#include "nccl_dyn.hpp"
 #include "program.hpp"
 
 namespace hshard::exec {
@@ -45,7 +44,7 @@ Context::Context(int rank, int world, int gpu, size_t arena_bytes)
 Context::~Context() {
   cudaSetDevice(gpu_);
   cudaDeviceSynchronize();
-  if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+  if (nccl_comm_) nccl::api().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (int r = 0; r < world_; ++r) {
     if (r == rank_) continue;
     if (peer_arena_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
@@ -126,8 +125,7 @@ void Context::nccl_init(const unsigned char id[128]) {
   std::memcpy(&uid, id, sizeof(uid));
   cuda_check(cudaSetDevice(gpu_), "cudaSetDevice");
   ncclComm_t comm;
-  const ncclResult_t r = ncclCommInitRank(&comm, world_, uid, rank_);
-  if (r != ncclSuccess) fail(Errc::CommError, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  nccl::check(nccl::api().CommInitRank(&comm, world_, uid, rank_), "ncclCommInitRank");
   nccl_comm_ = comm;
 }
 

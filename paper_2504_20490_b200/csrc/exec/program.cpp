@@ -26,9 +26,8 @@
 #include <set>
 #include <sstream>
 
-#include <nccl.h>
-
 #include "hshard_c.h"
+#include "nccl_dyn.hpp"
 #include "planner_internal.hpp"
 #include "program.hpp"
 
@@ -1139,18 +1138,16 @@ void Program::run(cudaStream_t s) {
     if (nccl_mode_ && p % 2 == 0 && !exchanges_[p / 2].empty()) {
       // the pack phase is followed by the phase's message exchange
       ncclComm_t comm = static_cast<ncclComm_t>(ctx_.nccl_comm());
-      auto nccl = [](ncclResult_t r, const char* what) {
-        if (r != ncclSuccess) fail(Errc::CommError, std::string(what) + ": " + ncclGetErrorString(r));
-      };
-      nccl(ncclGroupStart(), "ncclGroupStart");
+      const nccl::Api& n = nccl::api();
+      nccl::check(n.GroupStart(), "ncclGroupStart");
       for (const Exchange& x : exchanges_[p / 2]) {
         char* ptr = ctx_.arena() + x.offset;
         if (x.send)
-          nccl(ncclSend(ptr, x.bytes, ncclChar, x.peer, comm, s), "ncclSend");
+          nccl::check(n.Send(ptr, x.bytes, ncclChar, x.peer, comm, s), "ncclSend");
         else
-          nccl(ncclRecv(ptr, x.bytes, ncclChar, x.peer, comm, s), "ncclRecv");
+          nccl::check(n.Recv(ptr, x.bytes, ncclChar, x.peer, comm, s), "ncclRecv");
       }
-      nccl(ncclGroupEnd(), "ncclGroupEnd");
+      nccl::check(n.GroupEnd(), "ncclGroupEnd");
     }
     if (profiling_) event();
   }

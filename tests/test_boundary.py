@@ -10,6 +10,7 @@
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -65,3 +66,14 @@ def test_cpp_api_cpu():
 def test_cpp_api_gpu():
     res = subprocess.run([API_TEST, "gpu"], capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+def test_library_does_not_pin_nccl_before_torch():
+    """libhshard_b200.so must not link libnccl: loaded before torch it would bind
+    libnccl.so.2 to the system NCCL and break torch's own NCCL symbols."""
+    out = subprocess.run(["ldd", LIB_PATH], capture_output=True, text=True).stdout
+    assert "libnccl" not in out
+    res = subprocess.run([sys.executable, "-c",
+                          "import paper_2504_20490_b200, torch, torch.distributed; print('ok')"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
