@@ -1098,8 +1098,12 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
                      : std::max(1, std::min<int>(cnt, max_grid));
       if (l.tma) {
         stats_.tma_items += cnt;
-        // static round-robin for the first ~15/16 of the items, dynamic tail
-        l.tables.n_static = static_cast<int32_t>((static_cast<int64_t>(cnt) * 15 / 16) / l.grid * l.grid);
+        // Single GPU: items are uniform local work, a static round-robin is
+        // best (no atomic on the producer's critical path).  Multi-GPU: local
+        // and NVLink items differ in cost, so the last ~1/16 are dynamic.
+        l.tables.n_static = ctx_.world() == 1
+                                ? cnt
+                                : static_cast<int32_t>((static_cast<int64_t>(cnt) * 15 / 16) / l.grid * l.grid);
       }
       d.launches.push_back(l);
       ++launches;

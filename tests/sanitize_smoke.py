@@ -34,7 +34,7 @@ for src, dst, shape, dt in cases:
             bad += not np.array_equal(lay.read("dst", slot, dev), want[dev])
         prog.close()
         ctx.reset(mark)
-entries = [(t, s, d, tuple(max(8, x // 128) for x in sh)) for t, s, d, sh in W.config4().transitions[:12]]
+entries = [(t, s, d, tuple(max(8, x // 64) for x in sh)) for t, s, d, sh in W.config4().transitions[:12]]
 plan = H.plan_switch(entries, "bf16")
 lay = ShardLayout(ctx, plan, 8)
 lay.fill_src(6, "grid")
