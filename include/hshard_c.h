@@ -145,6 +145,13 @@ int hs_prog_phase_ms(hs_prog* prog, double* out, int n, int* runs);
  * run for this rank, task counts. */
 int hs_prog_stats(const hs_prog* prog, char** json);
 
+/* CPU-only dry run: compile `plan` for `rank` of `world` (virtual arenas, no
+ * CUDA) and return the program statistics and this rank's final task list
+ * as JSON (box, outputs, inputs, groups) -- how the multi-GPU partitioning is
+ * tested without GPUs. */
+int hs_analyze(const hs_plan* plan, int rank, int world, const int* v_to_rank, int n_virt, int flags,
+               char** stats_json, char** tasks_json);
+
 /* Deterministic counter-hash payload, written
  * into this rank's shard of virtual device `dev` for annotation `anno`. */
 int hs_fill_shard(hs_ctx* ctx, const char* anno, const int64_t* shape, int ndim, int dtype,

@@ -75,6 +75,7 @@ def _load() -> ctypes.CDLL:
         "hs_prog_stats": (c_int, [c_void_p, P(c_void_p)]),
         "hs_prog_profile": (c_int, [c_void_p, c_int]),
         "hs_prog_phase_ms": (c_int, [c_void_p, P(ctypes.c_double), c_int, P(c_int)]),
+        "hs_analyze": (c_int, [c_void_p, c_int, c_int, P(c_int), c_int, c_int, P(c_void_p), P(c_void_p)]),
         "hs_fill_shard": (c_int, [c_void_p, c_char_p, P(c_int64), c_int, c_int, c_int, c_size_t,
                                   c_uint32, c_int, c_int, c_void_p]),
         "hs_verify_shard": (c_int, [c_void_p, c_char_p, P(c_int64), c_int, c_int, c_int, c_size_t,

@@ -130,6 +130,43 @@ int hs_prog_stats(const hs_prog* prog, char** json) {
   return guarded([&] { *json = dup_string(prog->p->stats_json()); });
 }
 
+int hs_analyze(const hs_plan* plan, int rank, int world, const int* v_to_rank, int n_virt, int flags,
+               char** stats_json, char** tasks_json) {
+  return guarded([&] {
+    auto ctx = exec::Context::analysis(rank, world);
+    // every shard gets a distinct 256-byte-aligned virtual offset on its rank
+    const auto& comm = plan->comm;
+    std::vector<std::pair<const HetAnnotation*, const HetAnnotation*>> annos;
+    std::vector<Shape> shapes;
+    if (comm) {
+      annos.emplace_back(&comm->src, &comm->dst);
+      shapes.push_back(comm->shape);
+    } else {
+      for (const SwitchEntry& e : plan->sw->diff) {
+        annos.emplace_back(&e.src, &e.dst);
+        shapes.push_back(e.shape);
+      }
+    }
+    const size_t n = annos.size() * static_cast<size_t>(n_virt);
+    std::vector<size_t> src_off(n, SIZE_MAX), dst_off(n, SIZE_MAX);
+    size_t next = 0;
+    const int es = dtype_width(comm ? comm->dtype : plan->sw->dtype);
+    for (size_t t = 0; t < annos.size(); ++t)
+      for (int side = 0; side < 2; ++side)
+        for (const auto& [d, r] : placements(side ? *annos[t].second : *annos[t].first, shapes[t])) {
+          if (d < 0 || d >= n_virt) fail(Errc::UnknownDevice, "device without rank mapping");
+          (side ? dst_off : src_off)[t * n_virt + d] = next;
+          next += ((static_cast<size_t>(r.cells()) * es + 255) / 256) * 256;
+        }
+    ctx->alloc(next);
+    std::vector<int> map(v_to_rank, v_to_rank + n_virt);
+    exec::Program prog(*ctx, comm ? &*comm : nullptr, plan->sw ? &*plan->sw : nullptr, map,
+                       src_off.data(), dst_off.data(), flags);
+    *stats_json = dup_string(prog.stats_json());
+    *tasks_json = dup_string(prog.tasks_json());
+  });
+}
+
 int hs_fill_shard(hs_ctx* ctx, const char* anno, const int64_t* shape, int ndim, int dtype,
                   int device, size_t offset, uint32_t seed, int tensor_id, int mode, void* stream) {
   return guarded([&] {

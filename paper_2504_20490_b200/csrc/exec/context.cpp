@@ -41,7 +41,23 @@ Context::Context(int rank, int world, int gpu, size_t arena_bytes)
   cuda_check(cudaDeviceSynchronize(), "context init");
 }
 
+Context::Context(AnalysisTag, int rank, int world) : rank_(rank), world_(world), gpu_(-1) {
+  if (world < 1 || rank < 0 || rank >= world) fail(Errc::UnknownDevice, "bad rank/world");
+  analysis_ = true;
+  arena_bytes_ = size_t{1} << 44;
+  peer_arena_.resize(world);
+  for (int r = 0; r < world; ++r)  // disjoint, 4 KiB-aligned virtual bases
+    peer_arena_[r] = reinterpret_cast<char*>((uintptr_t{1} << 46) * static_cast<uintptr_t>(r + 1));
+  arena_ = peer_arena_[rank];
+  peers_open_ = true;
+}
+
+std::unique_ptr<Context> Context::analysis(int rank, int world) {
+  return std::unique_ptr<Context>(new Context(AnalysisTag{}, rank, world));
+}
+
 Context::~Context() {
+  if (analysis_) return;
   cudaSetDevice(gpu_);
   cudaDeviceSynchronize();
   if (nccl_comm_) nccl::api().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));

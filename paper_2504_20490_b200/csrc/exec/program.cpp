@@ -292,7 +292,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   if (nccl_mode_) {
     // baseline transport: plain pulls, no peer stores (the rewrites below
     // that store into peers are off); remote inputs are staged in stage_for_nccl()
-    if (!ctx_.nccl_comm()) fail(Errc::CommError, "HS_PROG_NCCL needs hs_ctx_nccl_init first");
+    if (!ctx_.nccl_comm() && !ctx_.is_analysis()) fail(Errc::CommError, "HS_PROG_NCCL needs hs_ctx_nccl_init first");
     flags_ |= HS_PROG_NO_RELAY | HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES;
     flags_ &= ~(HS_PROG_PUSH_ALL | HS_PROG_FUSE_PHASES);
   }
@@ -412,6 +412,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     }
     if (mine_task) mine.push_back(std::move(t));
   }
+  if (ctx_.is_analysis()) analysed_ = mine;
   for (const BoxTask& t : mine) {
     for (const Operand& o : t.dsts)
       if (loc(o.state, t.tensor, o.dev).offset == SIZE_MAX)
@@ -1071,10 +1072,13 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
                   ph[p].items[v].size() * sizeof(WorkItem));
     std::memcpy(host.data() + offs[p].recs, recs[p].data(), recs[p].size() * sizeof(uint4));
   }
-  cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
-  cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
-             "cudaMemcpy(tables)");
-  char* base = static_cast<char*>(dev_block_);
+  char* base = nullptr;
+  if (!ctx_.is_analysis()) {
+    cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
+    cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
+               "cudaMemcpy(tables)");
+    base = static_cast<char*>(dev_block_);
+  }
   dphases_.assign(n_phases_, {});
   const int max_grid = ctx_.sm_count() * kBlocksPerSm;
   int launches = 0;
@@ -1117,6 +1121,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
 
 // ---------------------------------------------------------------- run
 void Program::run(cudaStream_t s) {
+  if (ctx_.is_analysis()) fail(Errc::UnsupportedOp, "analysis programs do not run");
   if (!s) s = ctx_.stream();
   auto event = [&]() {
     if (events_used_ == events_.size()) {
@@ -1171,6 +1176,43 @@ void Program::run_host(const void* const* src_host, void* const* dst_host) {
   }
   cuda_check(cudaStreamSynchronize(s), "run_host sync");
   ctx_.check_barrier_error();
+}
+
+std::string Program::tasks_json() const {
+  auto kind = [this](int state) -> const char* {
+    if (state == 0) return "src";
+    if (state == static_cast<int>(final_state_)) return "dst";
+    if (state == mid_state_) return "mid";
+    if (state >= staging_state_) return state == staging_state_ ? "send" : "recv";
+    return "relay";
+  };
+  std::ostringstream o;
+  o << "[";
+  bool first = true;
+  for (const BoxTask& t : analysed_) {
+    o << (first ? "" : ",") << "{\"phase\":" << t.phase << ",\"tensor\":" << t.tensor << ",\"rank\":" << t.rank
+      << ",\"box\":[";
+    first = false;
+    for (size_t d = 0; d < t.box.bounds.size(); ++d)
+      o << (d ? "," : "") << "[" << t.box.bounds[d][0] << "," << t.box.bounds[d][1] << "]";
+    auto ops = [&](const std::vector<Operand>& v) {
+      o << "[";
+      for (size_t i = 0; i < v.size(); ++i) {
+        const ShardLoc& L = states_[v[i].state].at({t.tensor, v[i].dev});
+        o << (i ? "," : "") << "[\"" << kind(v[i].state) << "\"," << v[i].dev << "," << L.rank << "]";
+      }
+      o << "]";
+    };
+    o << "],\"dsts\":";
+    ops(t.dsts);
+    o << ",\"terms\":";
+    ops(t.terms);
+    o << ",\"groups\":[";
+    for (size_t g = 0; g < t.groups.size(); ++g) o << (g ? "," : "") << t.groups[g];
+    o << "]}";
+  }
+  o << "]";
+  return o.str();
 }
 
 std::string Program::stats_json() const {

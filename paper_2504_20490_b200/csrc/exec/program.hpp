@@ -25,6 +25,10 @@ class Context {
  public:
   Context(int rank, int world, int gpu, size_t arena_bytes);
   ~Context();
+  // CUDA-free context for plan analysis (hs_analyze): virtual arenas, no
+  // device memory; programs compiled against it build no device tables.
+  static std::unique_ptr<Context> analysis(int rank, int world);
+  bool is_analysis() const { return analysis_; }
 
   int rank() const { return rank_; }
   int world() const { return world_; }
@@ -69,6 +73,9 @@ class Context {
   bool peers_open_ = false;
   cudaStream_t stream_ = nullptr;
   void* nccl_comm_ = nullptr;  // ncclComm_t
+  bool analysis_ = false;
+  struct AnalysisTag {};
+  Context(AnalysisTag, int rank, int world);
 };
 
 // Where one tensor's shard for one virtual device lives in one layout state.
@@ -142,6 +149,8 @@ class Program {
   int phases() const { return n_phases_; }
   const ProgramStats& stats() const { return stats_; }
   std::string stats_json() const;
+  // Analysis contexts only: this rank's tasks after every rewrite.
+  std::string tasks_json() const;
   int dtype() const { return dtype_; }
 
  private:
@@ -197,6 +206,7 @@ class Program {
   std::vector<cudaEvent_t> events_;  // 2 per phase per profiled run
   size_t events_used_ = 0;
   ProgramStats stats_;
+  std::vector<BoxTask> analysed_;  // analysis contexts: this rank's final tasks
   // host-buffer path: (virtual device, tensor) -> (offset, bytes) on this rank
   std::vector<std::tuple<DeviceId, int, size_t, size_t>> host_src_, host_dst_;
 };

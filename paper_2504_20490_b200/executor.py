@@ -339,3 +339,13 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
         else:
             prog.close()
     return best, timings
+
+
+def analyze(plan: H.Plan, world: int, rank: int, n_virtual: int, flags: int = 0,
+            v_to_rank: Optional[Sequence[int]] = None):
+    """CPU-only dry run of the compiler for one rank (hs_analyze): (stats, tasks)."""
+    m = list(v_to_rank) if v_to_rank is not None else block_map(n_virtual, world)
+    arr = (c_int * n_virtual)(*m)
+    st, ts = c_void_p(), c_void_p()
+    check(LIB.hs_analyze(plan.handle, rank, world, arr, n_virtual, flags, ctypes.byref(st), ctypes.byref(ts)))
+    return json.loads(take_string(st)), json.loads(take_string(ts))

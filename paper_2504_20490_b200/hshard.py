@@ -115,7 +115,7 @@ class Plan:
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
-        if h:
+        if h and LIB is not None:  # module globals may already be gone at exit
             LIB.hs_plan_destroy(h)
 
 

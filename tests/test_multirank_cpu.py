@@ -1,0 +1,137 @@
+"""Multi-rank partitioning on CPU: the executor compiler's dry run (hs_analyze)
+per rank, under a real world-size-2 gloo process group and, in-process, for
+4 and 8 ranks.  Checks, for every BASELINE workload and program variant:
+
+* every destination cell is written exactly once by the union of all ranks'
+  tasks, in whichever phase finalises it (no gaps, no double writes);
+* every relay / intermediate buffer a task reads was written by an earlier
+  phase of some rank, and every NCCL receive slot by an earlier send of a peer;
+* NVLink bytes leaving all ranks equal the bytes arriving;
+* a task's outputs are on its own rank unless they are relay stores or pushed
+  (multi-output) results, never source shards.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from paper_2504_20490_b200 import hshard as H
+from paper_2504_20490_b200 import workloads as W
+from paper_2504_20490_b200.executor import analyze
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FLAG_SETS = [0, 14, 1, 32, 128, 256, 512, 1024, 1152, 2048, 2062]
+NAMES = ["cfg1A", "cfg1B", "cfg1C", "cfg1D", "cfg2e", "cfg2a", "cfg2b", "cfg2d", "cfg3b", "cfg3a",
+         "cfg3c", "cfg4"]
+
+
+def _plan(w):
+    if w.kind == "classify":
+        t, s, d, sh = w.transitions[0]
+        return H.classify(s, d, sh, w.dtype)
+    return H.plan_switch(w.transitions, w.dtype)
+
+
+def _boxes_tile(box, parts):
+    """parts exactly tile box: volumes add up and no two overlap."""
+    vol = lambda b: __import__("math").prod(hi - lo for lo, hi in b)
+    if sum(vol(p) for p in parts) != vol(box):
+        return False
+    for i in range(len(parts)):
+        for j in range(i + 1, len(parts)):
+            if all(max(a[0], b[0]) < min(a[1], b[1]) for a, b in zip(parts[i], parts[j])):
+                return False
+    return all(all(bl <= lo and hi <= bh for (lo, hi), (bl, bh) in zip(p, box)) for p in parts)
+
+
+def check_partition(w, plan, per_rank, world):
+    """per_rank: [(stats, tasks)] for every rank."""
+    stats = [s for s, _ in per_rank]
+    tasks = [t for _, ts in per_rank for t in ts]
+    assert sum(s["nvlink_in"] for s in stats) == sum(s["nvlink_out"] for s in stats)
+    # destination coverage
+    entries = ([(0, plan.meta["dst"], plan.meta["shape"])] if plan.kind == "comm"
+               else [(i, d, sh) for i, (tid, s, d, sh) in enumerate(plan.meta["entries"])])
+    written = {}
+    for t in tasks:
+        for kind, dev, rank in t["dsts"]:
+            if kind == "dst":
+                written.setdefault((t["tensor"], dev), []).append(t["box"])
+    for slot, dst, shape in entries:
+        for g in H.parse_annotation(dst)["groups"]:
+            for dev in g:
+                box = H.placement(dst, shape, dev)["bounds"]
+                assert _boxes_tile(box, written.get((slot, dev), [])), (w.name, slot, dev)
+    # relay / mid buffers are produced by an earlier phase before they are read
+    produced = {}
+    for t in tasks:
+        for kind, dev, rank in t["dsts"]:
+            if kind in ("relay", "mid"):
+                produced.setdefault((kind, t["tensor"], dev, rank), []).append((t["phase"], t["box"]))
+            if kind == "send":  # NCCL staging slot: one index space across ranks
+                produced.setdefault(("recv", t["tensor"], dev), []).append((t["phase"], t["box"], rank))
+    for t in tasks:
+        for kind, dev, rank in t["terms"]:
+            if kind == "relay":
+                assert rank == t["rank"], t
+            if kind in ("relay", "mid", "recv"):
+                if kind == "recv":
+                    cover = [b for ph, b, r in produced.get((kind, t["tensor"], dev), [])
+                             if ph < t["phase"] and r != t["rank"]]
+                else:
+                    cover = [b for ph, b in produced.get((kind, t["tensor"], dev, rank), []) if ph < t["phase"]]
+                inside = [[[max(lo, a), min(hi, b)] for (lo, hi), (a, b) in zip(c, t["box"])] for c in cover
+                          if all(max(lo, a) < min(hi, b) for (lo, hi), (a, b) in zip(c, t["box"]))]
+                assert _boxes_tile(t["box"], inside), (w.name, t)
+        for kind, dev, rank in t["dsts"]:
+            if rank != t["rank"]:
+                assert kind in ("relay", "dst", "mid"), t
+
+
+def _analyze_all(w, plan, world, flags):
+    return [analyze(plan, world, r, w.n_virtual, flags) for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_partitioning_in_process(world):
+    for name in NAMES:
+        w = W.by_name(name)
+        plan = _plan(w)
+        for flags in FLAG_SETS:
+            check_partition(w, plan, _analyze_all(w, plan, world, flags), world)
+
+
+def test_partitioning_gloo_world2(tmp_path):
+    """Two real processes (gloo): each compiles its own rank, results all-gathered."""
+    out = tmp_path / "res"
+    code = f"""
+import json, os, sys
+sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r})
+import torch.distributed as dist
+from paper_2504_20490_b200 import workloads as W
+from paper_2504_20490_b200.executor import analyze
+from test_multirank_cpu import NAMES, FLAG_SETS, _plan, check_partition
+dist.init_process_group('gloo')
+rank, world = dist.get_rank(), dist.get_world_size()
+ok = True
+for name in NAMES:
+    w = W.by_name(name); plan = _plan(w)
+    for flags in FLAG_SETS:
+        mine = analyze(plan, world, rank, w.n_virtual, flags)
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        if rank == 0:
+            check_partition(w, plan, allr, world)
+if rank == 0:
+    open({str(out)!r}, 'w').write('ok')
+dist.destroy_process_group()
+"""
+    script = tmp_path / "worker.py"
+    script.write_text(code)
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr=127.0.0.1", "--master-port=29641", str(script)],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-4000:]
+    assert out.read_text() == "ok"
