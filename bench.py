@@ -376,6 +376,12 @@ def main():
                                              "hbm_write": sst["hbm_write"], "nvlink_in": sst["nvlink_in"],
                                              "nvlink_out": sst["nvlink_out"], "items": sst["items"]})
                 line["ranks"] = per
+            from paper_2504_20490_b200.accounting import bus_bytes
+            rs = line.get("ranks") or [sst]
+            fl = max(max((r["hbm_read"] + r["hbm_write"]) / (peak * 1e9),
+                         max(r["nvlink_in"], r["nvlink_out"]) / (NVLINK_GBS * 1e9)) for r in rs) * 1e3
+            line["floor"] = {"ms": fl, "frac": fl / sms}
+            line["bus_gbs"] = max(bus_bytes(splan).values(), default=0) / (sms * 1e-3) / 1e9
             if rank == 0:
                 print(json.dumps(line), flush=True)
             del sprog, slay
@@ -428,6 +434,26 @@ def main():
                 "kernel": f"box_phase_kernel phase {dom}", "bytes_per_launch": nvin,
                 "launch_ms": phase_ms[dom], "hbm_achieved": (rd + wr) / kern_s / 1e9,
                 "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)"}
+
+    # ---- NCCL-convention bus GB/s, and the step
+    # floor = max over GPUs of max(NVLink bytes / link peak, HBM bytes / HBM
+    # peak) from each rank's compiled-program byte accounting.
+    from paper_2504_20490_b200.accounting import bus_bytes
+    bus = bus_bytes(plan)
+    bus_max = max(bus.values()) if bus else 0
+    mine = {"hbm": st["hbm_read"] + st["hbm_write"], "nv": max(st["nvlink_in"], st["nvlink_out"])}
+    per_rank = [mine]
+    if world > 1:
+        import torch.distributed as dist
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+    floor_ms = max(max(r["hbm"] / (peak * 1e9), r["nv"] / (NVLINK_GBS * 1e9)) for r in per_rank) * 1e3
+    floor = {"ms": floor_ms, "frac": floor_ms / ms, "hbm_peak_gbs": peak, "nvlink_peak_gbs": NVLINK_GBS,
+             "per_rank_hbm_bytes": [r["hbm"] for r in per_rank],
+             "per_rank_nvlink_bytes": [r["nv"] for r in per_rank],
+             "basis": "compiled program's per-rank bytes (src read once, dst written once, relays)"}
+    busd = {"gbs": bus_max / (ms * 1e-3) / 1e9, "bytes_max_device": bus_max,
+            "convention": "NCCL bus bytes per virtual device (accounting.py), max over devices / step time"}
 
     # ---- e2e through the host-buffer C-ABI path (pinned host memory)
     src_host, dst_host, keep = {}, {}, []
@@ -499,7 +525,7 @@ def main():
                        "program": {k: st[k] for k in ("phases", "plan_phases", "tasks", "items",
                                                       "fused_tasks", "tma_items", "hbm_read",
                                                       "hbm_write", "nvlink_in", "nvlink_out")}},
-            "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            "roofline": roof, "floor": floor, "bus": busd, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": args.steps * st["kernels_per_run"],
             "kernels_per_step": st["kernels_per_run"], "phase_ms": phase_ms,
             "verified": verified, "clocks": clk, "graph_switch": switch,
