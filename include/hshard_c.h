@@ -123,7 +123,12 @@ enum {
   HS_PROG_PUSH_ALL = 1024,        /* world > 1: every copy runs on its input's rank */
   HS_PROG_NCCL = 2048             /* world > 1: baseline transport -- remote inputs are packed,
                                      exchanged with grouped ncclSend/ncclRecv, and read locally
-                                     (no peer-memory access, no device barriers) */
+                                     (no peer-memory access, no device barriers) */,
+  HS_PROG_NO_STREAM = 4096,       /* world > 1: two-phase programs keep a barrier between the
+                                     phases instead of one launch with per-chunk ready flags */
+  HS_PROG_PULL_MID = 8192         /* world > 1: phase 2 pulls remote mid boxes from the
+                                     producer's HBM (local groups still fused) instead of
+                                     relay stores into the consumer's HBM */
 };
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);

@@ -23,6 +23,8 @@ namespace {
 constexpr int kBlock = 512;     // register path
 constexpr int kConsumerWarps = 16;                   // 512 consumer threads
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);  // + 1 producer warp
+constexpr int kDynThreads = kTmaThreads + 32;           // multi-GPU kernel: + 1 signaller warp
+constexpr int kSigRing = 64;                            // signaller queue slots
 
 // ---------------------------------------------------------------- arithmetic
 template <class T>
@@ -323,14 +325,107 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Streamed launches, signalling side.  A system-scope fence in an SM that is
+// streaming costs microseconds (it waits for the SM's outstanding memory
+// traffic), so consumer warps never issue one: each consumer warp of an item
+// of a signalling task orders its stores with fence.cta and counts itself in
+// shared memory; the item's last warp queues the task's SigDesc index in a
+// shared ring.  A dedicated signaller warp drains the ring in batches: one
+// fence.sc.sys per batch (cumulative over every queued item's stores, which
+// it acquired through the ring), then per entry one add to the task's item
+// counter and -- when that add completes the task's run -- red.release.sys
+// on every consumer flag.
+struct SigRing {
+  unsigned int cnt[kTmaStages];  // consumer warps done with the stage's item
+  unsigned int slot[kSigRing];   // SigDesc index + 1; 0 = empty
+  unsigned int tail;             // next slot to fill
+  unsigned int consumers_done;   // consumer warps that have exited
+};
+
+__device__ __forceinline__ void tma_count(SigRing* ring, int s, int sig, int lane) {
+  __threadfence_block();
+  __syncwarp();
+  if (lane == 0 && atomicAdd(&ring->cnt[s], 1u) == kConsumerWarps - 1) {
+    ring->cnt[s] = 0;
+    const unsigned int k = atomicAdd(&ring->tail, 1u) % kSigRing;
+    volatile unsigned int* v = ring->slot + k;
+    while (*v != 0) __nanosleep(64);  // ring full: the signaller is a batch behind
+    __threadfence_block();
+    *v = static_cast<unsigned int>(sig) + 1;
+  }
+  __syncwarp();
+}
+
+__device__ void tma_signaller(const PhaseTables& t, SigRing* ring, int lane) {
+  unsigned int head = 0;
+  while (true) {
+    volatile unsigned int* v = ring->slot + (head + lane) % kSigRing;
+    const unsigned int e = *v;
+    // consecutive ready entries from head
+    const unsigned int ready = __ballot_sync(0xffffffffu, e != 0);
+    const int n = __ffs(~ready) - 1 < 0 ? 32 : __ffs(~ready) - 1;
+    if (n == 0) {
+      // consumer warps queue every item before they exit, so once all have
+      // exited an empty head slot means the ring is drained
+      if (*reinterpret_cast<volatile unsigned int*>(&ring->consumers_done) == kConsumerWarps) {
+        __threadfence_block();
+        if (__ballot_sync(0xffffffffu, *v != 0) == 0) return;
+      } else {
+        __nanosleep(128);
+      }
+      continue;
+    }
+    __threadfence_system();
+    if (lane < n) {
+      *v = 0;
+      const SigDesc d = t.sigs[e - 1];
+      const unsigned long long old = atomicAdd(&t.done[d.done], 1ull);
+      if ((old + 1) % d.expected == 0)
+        for (uint32_t k = 0; k < d.ntargets; ++k)
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(t.targets[d.target0 + k]) : "memory");
+    }
+    head += n;
+    __syncwarp();
+  }
+}
+
+// Streamed launches: the producer warp's lane 0 waits until a consumer
+// piece's producers have all signalled this run; bounded by ~10 s, after
+// which it records DeadlockDetected and proceeds (never a hang).
+__device__ __forceinline__ void tma_wait(const PhaseTables& t, int flag, int need) {
+  const unsigned int want = t.epoch * static_cast<unsigned int>(need);
+  const unsigned int* f = t.wait_flags + flag;
+  unsigned long long t0 = 0;
+  const unsigned long long tw0 = t.trace ? global_ns() : 0;
+  while (true) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (static_cast<int>(v - want) >= 0) break;
+    if (t0 == 0) t0 = global_ns();
+    if (*reinterpret_cast<volatile int*>(t.error)) break;  // an earlier wait already gave up
+    if (global_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
+      *t.error = 1;
+      break;
+    }
+  }
+  // the TMA (async proxy) loads that follow read what peers stored
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (t.trace) {  // debug timeline: total and count of waits that spun
+    unsigned long long* tr = t.trace + blockIdx.x * 8;
+    tr[3] += global_ns() - tw0;
+    tr[4] += t0 != 0;
+  }
+}
+
 // One consumer-warp pass over pipeline stage `iter`: wait for it, form every
 // output vector of the item from shared memory, release the stage.  Returns
 // false on the producer's end marker.
 template <class T>
 __device__ __forceinline__ bool tma_consume(const unsigned char* stage, const uint4* meta,
-                                            uint64_t* full, uint64_t* empty, int iter, int lane) {
+                                            uint64_t* full, uint64_t* empty, SigRing* ring, int iter,
+                                            int lane) {
   const int ctid = threadIdx.x - 32;
-  constexpr int nct = kTmaThreads - 32;
+  constexpr int nct = 32 * kConsumerWarps;
   const int s = iter % kTmaStages;
   mbar_wait(&full[s], (iter / kTmaStages) & 1);
   const uint4* m = meta + s * 32;
@@ -356,57 +451,106 @@ __device__ __forceinline__ bool tma_consume(const unsigned char* stage, const ui
     }
     for (int o = 0; o < no; ++o) __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
   }
+  const int sig = h->sig;  // read before the stage is released
   __syncwarp();
+  if (sig >= 0) tma_count(ring, s, sig, lane);
   if (lane == 0) mbar_arrive(&empty[s]);
   return true;
 }
 
 template <class T>
-__global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTables t) {
+__global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTables t) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* stage = smem;
   uint4* meta = reinterpret_cast<uint4*>(smem + kTmaStages * kStageBytes);  // 32 words per stage
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + kTmaStages * 32);
   uint64_t* empty = full + kTmaStages;
+  SigRing* ring = reinterpret_cast<SigRing*>(empty + kTmaStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
+      ring->cnt[s] = 0;
     }
+    for (int k = 0; k < kSigRing; ++k) ring->slot[k] = 0;
+    ring->tail = 0;
+    ring->consumers_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int W = t.rec_words;
 
+  if (warp == kConsumerWarps + 1) {  // ---- signaller warp
+    if (t.sigs) tma_signaller(t, ring, lane);
+    return;
+  }
+
   if (warp == 0) {
     // ---- producer warp: the item record is prefetched one item ahead (one
     // 16-byte word per lane); lane k then streams term k's rows.
     // Items [0, n_static) are dealt round-robin (no dependency: the record is
-    // prefetched one item ahead); the tail is handed out dynamically (one
-    // atomic per item) so CTAs that drew cheap items keep pulling work.
+    // prefetched one item ahead); the rest are handed out dynamically (one
+    // atomic per item) from two queues (PhaseTables::n_first / first_ctas).
     const unsigned full_mask = 0xffffffffu;
-    auto next_item = [&](int prev, int iter_next) {
-      const int st = blockIdx.x + iter_next * static_cast<int>(gridDim.x);
-      if (st < t.n_static) return st;
-      int d = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
-      return t.n_static + __shfl_sync(full_mask, d, 0);
+    const bool first_role = static_cast<int>(blockIdx.x) < t.first_ctas;
+    unsigned long long* tr = t.trace ? t.trace + blockIdx.x * 8 : nullptr;
+    if (tr && lane == 0) {
+      tr[0] = global_ns();
+      tr[2] = 0; tr[3] = 0; tr[4] = 0; tr[5] = 0; tr[6] = 0;  // [6] unused
+      tr[7] = first_role;
+    }
+    // Tickets: lane 0 takes item i+2's index (an atomic) while item i is
+    // issued and resolves it one iteration later, so neither the atomic nor
+    // the record load that depends on it sits on the critical path.  A
+    // first-queue ticket that comes back past n_first is exchanged for a
+    // second-queue one (so a CTA never takes a first-queue item after a
+    // second-queue one).
+    bool first_open = first_role;
+    int k_static = 0;
+    auto issue = [&]() -> int {  // lane 0 only; encoded: >= 0 final, < 0 first-queue ticket
+      const int st = blockIdx.x + k_static * static_cast<int>(gridDim.x);
+      if (st < t.n_static) {
+        ++k_static;
+        return st;
+      }
+      if (first_open) return -1 - (t.n_static + atomicAdd(&t.sched[0], 1));
+      return t.n_first + atomicAdd(&t.sched[2], 1);
     };
-    int it = next_item(-1, 0);
+    auto resolve = [&](int ticket) -> int {  // all lanes
+      int d = ticket;
+      if (lane == 0 && d < 0) {
+        d = -1 - d;
+        if (d >= t.n_first) {
+          first_open = false;
+          d = t.n_first + atomicAdd(&t.sched[2], 1);
+          if (tr && tr[5] == 0) tr[5] = global_ns();
+        }
+      }
+      return __shfl_sync(full_mask, d, 0);
+    };
+    int it = resolve(lane == 0 ? issue() : 0);
     uint4 next = make_uint4(0, 0, 0, 0);
-    if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+    int pend = 0;
+    if (it < t.n_items) {
+      if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+      if (lane == 0) pend = issue();
+    }
     for (int iter = 0;; ++iter) {
       const int cur_it = it;
       const uint4 cur = next;
       if (cur_it < t.n_items) {
-        const int nxt = next_item(cur_it, iter + 1);
-        it = nxt;
-        if (nxt < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nxt) * W + lane];
+        it = resolve(pend);
+        if (it < t.n_items) {
+          if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+          if (lane == 0) pend = issue();
+        }
       }
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
       uint4* m = meta + s * 32;
       if (cur_it >= t.n_items) {  // end marker for the consumers
+        if (tr && lane == 0) { tr[1] = global_ns(); tr[2] = iter; }
         if (lane == 0) {
           reinterpret_cast<TmaRecHead*>(m)->nterms = -1;
           mbar_arrive_expect_tx(&full[s], 0);
@@ -414,6 +558,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
           if (atomicAdd(&t.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
             t.sched[0] = 0;
             t.sched[1] = 0;
+            t.sched[2] = 0;
           }
         }
         return;
@@ -421,6 +566,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
       if (lane < W) m[lane] = cur;
       __syncwarp();
       const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
+      if (h->wait >= 0) {
+        if (lane == 0) tma_wait(t, h->wait, h->need);
+        __syncwarp();
+      }
       const int nt = h->nterms, nrow = h->nrow;
       const uint32_t row_bytes = static_cast<uint32_t>(h->nvcol) * 16;
       if (lane == 0) mbar_arrive_expect_tx(&full[s], row_bytes * nrow * nt);  // release: meta
@@ -435,7 +584,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_kernel(PhaseTabl
 
   // ---- consumers (until the producer's end marker)
   for (int iter = 0;; ++iter)
-    if (!tma_consume<T>(stage, meta, full, empty, iter, lane)) break;
+    if (!tma_consume<T>(stage, meta, full, empty, ring, iter, lane)) break;
+  __threadfence_block();
+  if (lane == 0) atomicAdd(&ring->consumers_done, 1u);
 }
 
 // Single-GPU variant (items dealt round-robin, no scheduler state): the
@@ -676,6 +827,7 @@ cudaError_t by_dtype(int dtype, dim3 grid, dim3 block, cudaStream_t s, Args... a
 
 constexpr size_t kTmaSmem = kTmaStages * kStageBytes + kTmaStages * 32 * sizeof(uint4) +
                             2 * kTmaStages * sizeof(uint64_t);
+constexpr size_t kDynSmem = kTmaSmem + sizeof(SigRing);
 
 template <class T>
 struct PhaseK {
@@ -698,7 +850,7 @@ struct PhaseK {
     if (tma) {
       static bool configured = [] {
         cudaFuncSetAttribute(box_phase_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kTmaSmem));
+                             static_cast<int>(kDynSmem));
         cudaFuncSetAttribute(box_phase_tma_static_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kTmaSmem));
         return true;
@@ -707,7 +859,7 @@ struct PhaseK {
       if (t.n_static >= t.n_items)
         box_phase_tma_static_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       else
-        box_phase_tma_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+        box_phase_tma_kernel<T><<<g, dim3(kDynThreads), kDynSmem, s>>>(t);
       return;
     }
     if (reduce)

@@ -53,7 +53,10 @@ struct WorkItem {
 //   TmaRecHead, then (nterms + nout) TmaOperand: terms first, then outputs.
 struct TmaRecHead {
   int32_t nterms, nout, ngroups, nrow;
-  int32_t nvcol, pad0, pad1, pad2;
+  int32_t nvcol;
+  int32_t wait;  // streamed launches: flag index this item waits on (-1: none)
+  int32_t sig;   // streamed launches: SigDesc index signalled when its task is done (-1: none)
+  int32_t need;  // producer pieces the waited-on flag counts per run
   uint8_t gsize[16];
 };
 struct TmaOperand {
@@ -63,15 +66,40 @@ struct TmaOperand {
 inline constexpr int kTmaHeadWords = sizeof(TmaRecHead) / 16;                 // 3
 inline constexpr int kTmaMaxWords = kTmaHeadWords + kMaxTerms + kMaxOuts;    // 27 <= 32 lanes
 
+// Streamed launches (both plan phases in one launch, no barrier between):
+// a producer task's last finished item adds 1 (red.release.sys) to the flag
+// of every consumer piece that reads its output, on the consumer's rank; a
+// consumer item's producer warp waits (ld.acquire.sys) until its flag reaches
+// epoch * need before loading.
+struct SigDesc {
+  uint32_t done;      // index of this task's item counter in PhaseTables::done
+  uint32_t expected;  // TMA items of the task per run
+  uint32_t target0;   // first flag pointer in PhaseTables::targets
+  uint32_t ntargets;
+};
+
 struct PhaseTables {
   const TaskDesc* tasks;
   const TermDesc* terms;
   const WorkItem* items;  // register path
   const uint4* recs;      // TMA path: n_items slots of rec_words 16-byte words
-  int* sched;             // TMA path: {next item, finished CTAs}; zero between launches
+  int* sched;             // TMA path: {next first-queue item, finished CTAs, next second-queue
+                          // item, pad}; zero between launches
   int32_t n_items;
   int32_t rec_words;
   int32_t n_static;       // TMA path: items [0, n_static) are dealt round-robin
+  // TMA path queues: items [0, n_first) never wait; [n_first, n_items) may.
+  // CTAs [0, first_ctas) drain the first queue, then the second; the others
+  // take only the second, so no item that signals is ever queued behind a wait.
+  int32_t n_first;
+  int32_t first_ctas;
+  uint32_t epoch;                    // run number (streamed launches)
+  const SigDesc* sigs;
+  unsigned int* const* targets;      // flag addresses, possibly on peers
+  unsigned long long* done;          // per signalling task: items finished, all runs
+  const unsigned int* wait_flags;    // this rank's flags
+  int* error;                        // set when a wait times out (DeadlockDetected)
+  unsigned long long* trace;         // debug (HS_TRACE): 8 globaltimer words per CTA, or null
 };
 
 // Shared-memory staging of the TMA kernel: kStages ring buffers of

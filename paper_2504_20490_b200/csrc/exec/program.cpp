@@ -20,11 +20,13 @@
 //   * output merging: tasks with identical inputs (replicas, SplitAG fan-out)
 //     become one task with several outputs, so inputs are read once.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
 #include <set>
 #include <sstream>
+#include <tuple>
 
 #include "hshard_c.h"
 #include "nccl_dyn.hpp"
@@ -337,7 +339,9 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     // fuses its local groups too (least HBM traffic) unless
     // HS_PROG_RELAY_KEEP_LOCAL asks to compute them before the barrier,
     // concurrently with the remote producers.
-    const RelayMode mode = (flags_ & HS_PROG_RELAY_KEEP_LOCAL) ? RelayMode::KeepLocal : RelayMode::FuseLocal;
+    const RelayMode mode = (flags_ & HS_PROG_PULL_MID)           ? RelayMode::Pull
+                           : (flags_ & HS_PROG_RELAY_KEEP_LOCAL) ? RelayMode::KeepLocal
+                                                                 : RelayMode::FuseLocal;
     tasks = finish(fuse_phases(std::move(tasks), mode));
     stats_.model_ms[0] = estimate_seconds(tasks, n_phases_) * 1e3;
   } else {
@@ -345,6 +349,18 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   }
 
   if (nccl_mode_) stage_for_nccl(tasks);
+
+  // world > 1: both plan phases in one launch with per-chunk ready flags
+  // (kept only if every producer / consumer piece runs on the TMA path).
+  std::vector<BoxTask> unstreamed;
+  if (ctx_.world() > 1 && n_phases_ == 2 && !nccl_mode_ && !(flags_ & (HS_PROG_NO_STREAM | HS_PROG_NO_TMA))) {
+    std::vector<BoxTask> st = stream_phases(tasks);
+    if (!st.empty()) {
+      unstreamed = std::move(tasks);
+      tasks = std::move(st);
+      streamed_ = true;
+    }
+  }
 
   // Symmetric placement of the intermediate (mid) and relay shards still in
   // use: every rank packs its own densely from one common base.
@@ -370,10 +386,37 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     }
   }
 
+  if (streamed_) {
+    bool ok = true;
+    for (const BoxTask& t : tasks)
+      if ((t.wait >= 0 || !t.targets.empty()) && !tma_capable(t)) ok = false;
+    if (!ok) {
+      tasks = std::move(unstreamed);
+      streamed_ = false;
+    } else {
+      n_phases_ = 1;
+      // symmetric flag array (same offset on every rank), zeroed before the
+      // first run's opening barrier
+      std::vector<int> nflags(ctx_.world(), 0);
+      for (const BoxTask& t : tasks)
+        if (t.wait >= 0) nflags[t.rank] = std::max(nflags[t.rank], t.wait + 1);
+      const size_t bytes = static_cast<size_t>(*std::max_element(nflags.begin(), nflags.end())) * 4;
+      flag_off_ = ctx_.alloc(bytes + 256);
+      if (!ctx_.is_analysis()) {
+        cuda_check(cudaMemsetAsync(ctx_.arena() + flag_off_, 0, bytes + 256, ctx_.stream()), "memset(flags)");
+        cuda_check(cudaStreamSynchronize(ctx_.stream()), "memset(flags) sync");
+      }
+    }
+  }
+  stats_.streamed = streamed_;
+
+  // Stores into peers' destination shards in the last launch need a closing
+  // barrier (relay / intermediate stores are consumed inside the run).
   for (const BoxTask& t : tasks)
     if (t.phase == n_phases_ - 1)
       for (const Operand& o : t.dsts)
-        remote_final_writes_ = remote_final_writes_ || rank_of(o, t.tensor) != t.rank;
+        remote_final_writes_ = remote_final_writes_ ||
+                               (o.state == static_cast<int>(final_state_) && rank_of(o, t.tensor) != t.rank);
 
   // ---- algorithmic byte accounting over ALL ranks' tasks, then keep ours
   const int me = ctx_.rank();
@@ -531,7 +574,7 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
             for (const Operand& in : tasks[p].terms) fusable = fusable && rank_of(in, T.tensor) == q;
         }
       if (relay && rank_of(o, T.tensor) != q)
-        pol[j] = RELAY;
+        pol[j] = mode == RelayMode::Pull ? KEEP : RELAY;
       else if (fusable && !prod[j].empty())
         pol[j] = FUSE;
     }
@@ -876,11 +919,170 @@ std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks) {
   return out;
 }
 
+// ---------------------------------------------------------------- streaming
+// world > 1, two plan phases: ONE launch instead of phase / barrier / phase.
+// Producer tasks (phase 0, an output a phase-1 task reads) and their consumers
+// are cut along dim 0 at common multiples of ~kChunkBytes of the operand's
+// rows.  Every consumer piece gets a ready flag on its rank; each producer
+// piece it reads adds 1 to that flag once per run when its last item has
+// landed (kernels.cuh SigDesc), and the consumer's loads wait for
+// epoch * need.  Results are unchanged: the same tasks, cut, run in the same
+// order of terms.  Returns {} when no phase-1 task reads a phase-0 output.
+std::vector<BoxTask> Program::stream_phases(const std::vector<BoxTask>& in) {
+  using Key = std::tuple<int, int, DeviceId>;  // (state, tensor, device)
+  auto key = [](const BoxTask& t, const Operand& o) { return Key{o.state, t.tensor, o.dev}; };
+  int64_t chunk_bytes = 2 << 20;
+  if (const char* e = std::getenv("HS_STREAM_CHUNK_KB")) chunk_bytes = std::max(1L, std::atol(e)) << 10;
+
+  std::map<Key, std::vector<int>> writers;
+  for (int i = 0; i < static_cast<int>(in.size()); ++i)
+    if (in[i].phase == 0)
+      for (const Operand& o : in[i].dsts) writers[key(in[i], o)].push_back(i);
+  std::map<Key, int64_t> rows;  // chunk rows of each operand read across the phases
+  std::vector<int64_t> cut_rows(in.size(), 0);
+  auto note = [&](int i, const Key& k) {
+    auto [it, fresh] = rows.try_emplace(k, 0);
+    if (fresh) {
+      const ShardLoc& L = loc(std::get<0>(k), std::get<1>(k), std::get<2>(k));
+      int64_t row_bytes = es_;
+      for (size_t d = 1; d < L.region.bounds.size(); ++d) row_bytes *= L.region.bounds[d][1] - L.region.bounds[d][0];
+      it->second = std::max<int64_t>(1, chunk_bytes / row_bytes);
+    }
+    cut_rows[i] = cut_rows[i] ? std::min(cut_rows[i], it->second) : it->second;
+  };
+  bool any = false;
+  for (int i = 0; i < static_cast<int>(in.size()); ++i) {
+    if (in[i].phase != 1) continue;
+    for (const Operand& o : in[i].terms) {
+      auto it = writers.find(key(in[i], o));
+      if (it == writers.end()) continue;
+      for (int p : it->second)
+        if (intersect(in[p].box, in[i].box)) {
+          note(i, it->first);
+          note(p, it->first);
+          any = true;
+        }
+    }
+  }
+  if (!any) return {};
+
+  std::vector<BoxTask> out;
+  for (int i = 0; i < static_cast<int>(in.size()); ++i) {
+    const BoxTask& T = in[i];
+    const int64_t R = cut_rows[i];
+    const int64_t lo = T.box.bounds[0][0], hi = T.box.bounds[0][1];
+    if (!R || hi - lo <= R) {
+      out.push_back(T);
+      continue;
+    }
+    for (int64_t a = lo; a < hi;) {
+      const int64_t b = std::min(hi, (a / R + 1) * R);
+      BoxTask piece = T;
+      piece.box.bounds[0] = {a, b};
+      out.push_back(std::move(piece));
+      a = b;
+    }
+  }
+  std::map<Key, std::vector<int>> w2;
+  for (int j = 0; j < static_cast<int>(out.size()); ++j)
+    if (out[j].phase == 0)
+      for (const Operand& o : out[j].dsts) w2[key(out[j], o)].push_back(j);
+  std::vector<int> flags(ctx_.world(), 0);
+  for (int j = 0; j < static_cast<int>(out.size()); ++j) {
+    if (out[j].phase != 1) continue;
+    std::set<int> deps;
+    for (const Operand& o : out[j].terms) {
+      auto it = w2.find(key(out[j], o));
+      if (it == w2.end()) continue;
+      for (int p : it->second)
+        if (intersect(out[p].box, out[j].box)) deps.insert(p);
+    }
+    if (deps.empty()) continue;
+    out[j].wait = flags[out[j].rank]++;
+    out[j].need = static_cast<int>(deps.size());
+    for (int p : deps) out[p].targets.emplace_back(out[j].rank, out[j].wait);
+  }
+  for (BoxTask& t : out) t.phase = 0;
+  return out;
+}
+
+// A task's box with unit outer dims dropped and dims contiguous for every
+// operand merged (outputs first, then terms): what the device tables hold.
+struct Program::Flat {
+  std::vector<int64_t> ext;                // outermost first
+  std::vector<std::vector<int64_t>> st;    // per operand: element strides
+  std::vector<const ShardLoc*> locs;
+  std::vector<int64_t> elem_off;           // per operand: box origin in its shard
+  int vec_bytes = 0;                       // widest vector legal for every operand
+};
+
+Program::Flat Program::flatten(const BoxTask& bt) {
+  Flat f;
+  std::vector<std::vector<int64_t>> full;
+  auto add = [&](const Operand& o) {
+    const ShardLoc& L = loc(o.state, bt.tensor, o.dev);
+    full.push_back(row_major_strides(L.region.extents()));
+    int64_t off = 0;
+    for (size_t i = 0; i < bt.box.bounds.size(); ++i) off += (bt.box.bounds[i][0] - L.region.bounds[i][0]) * full.back()[i];
+    f.locs.push_back(&L);
+    f.elem_off.push_back(off);
+  };
+  for (const Operand& o : bt.dsts) add(o);
+  for (const Operand& o : bt.terms) add(o);
+  const Shape box = bt.box.extents();
+  const size_t nd = box.size();
+  f.st.resize(full.size());
+  for (size_t i = 0; i < nd; ++i) {
+    if (box[i] == 1 && i + 1 < nd) continue;  // the innermost (stride-1) dim always stays
+    f.ext.push_back(box[i]);
+    for (size_t k = 0; k < full.size(); ++k) f.st[k].push_back(full[k][i]);
+  }
+  for (int i = static_cast<int>(f.ext.size()) - 2; i >= 0; --i) {
+    bool merge = true;
+    for (size_t k = 0; k < full.size(); ++k) merge = merge && f.st[k][i] == f.ext[i + 1] * f.st[k][i + 1];
+    if (!merge) continue;
+    f.ext[i] *= f.ext[i + 1];
+    f.ext.erase(f.ext.begin() + i + 1);
+    for (auto& s : f.st) {
+      s[i] = s[i + 1];
+      s.erase(s.begin() + i + 1);
+    }
+  }
+  if (f.ext.empty()) {
+    f.ext.push_back(1);
+    for (auto& s : f.st) s.push_back(1);
+  }
+  // Alignment from arena offsets: every rank's arena base is 256-byte aligned.
+  const int rd = static_cast<int>(f.ext.size());
+  auto ok = [&](int v) {
+    if ((f.ext.back() * es_) % v) return false;
+    for (size_t k = 0; k < f.locs.size(); ++k) {
+      if ((f.locs[k]->offset + f.elem_off[k] * es_) % v) return false;
+      for (int j = 0; j + 1 < rd; ++j)
+        if ((f.st[k][j] * es_) % v) return false;
+    }
+    return true;
+  };
+  int vb = 16;
+  while (vb > es_ && !ok(vb)) vb /= 2;
+  f.vec_bytes = std::max(vb, es_);
+  return f;
+}
+
+bool Program::tma_capable(const BoxTask& bt) {
+  const Flat f = flatten(bt);
+  bool all_local = true;
+  for (const ShardLoc* L : f.locs) all_local = all_local && L->rank == bt.rank;
+  return f.vec_bytes == 16 && (all_local || !(flags_ & HS_PROG_NO_TMA_PEER)) && !(flags_ & HS_PROG_NO_TMA) &&
+         f.ext.size() <= 4;
+}
+
 // ---------------------------------------------------------------- tables
 void Program::build_tables(const std::vector<BoxTask>& tasks) {
   struct Host {
     std::vector<TaskDesc> tasks;
     std::vector<TermDesc> terms;
+    std::vector<const BoxTask*> src;  // the BoxTask of each TaskDesc
     // [0] TMA; [1..4] register copy/zero by width 16, 8, 4, 2; [5..8] register reduce
     std::vector<WorkItem> items[kSlots];
   };
@@ -889,77 +1091,20 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   };
   std::vector<Host> ph(n_phases_);
   stats_.phases = n_phases_;
-  const int me = ctx_.rank();
 
   for (const BoxTask& bt : tasks) {
     Host& H = ph.at(bt.phase);
     if (static_cast<int>(bt.terms.size()) > kMaxTerms) fail(Errc::UnsupportedOp, "more than 16 terms in one task");
     if (static_cast<int>(bt.dsts.size()) > kMaxOuts) fail(Errc::UnsupportedOp, "more than 8 outputs in one task");
-    // refs: outputs then terms
-    struct Ref {
-      const ShardLoc* L;
-      std::vector<int64_t> st;
-      int64_t elem_off;
-    };
-    std::vector<Ref> refs;
-    auto add_ref = [&](const Operand& o) {
-      const ShardLoc& L = loc(o.state, bt.tensor, o.dev);
-      Ref r{&L, row_major_strides(L.region.extents()), 0};
-      for (size_t i = 0; i < bt.box.bounds.size(); ++i)
-        r.elem_off += (bt.box.bounds[i][0] - L.region.bounds[i][0]) * r.st[i];
-      refs.push_back(std::move(r));
-    };
-    for (const Operand& o : bt.dsts) add_ref(o);
-    for (const Operand& o : bt.terms) add_ref(o);
+    const Flat f = flatten(bt);
     const size_t nout = bt.dsts.size();
-    const Shape box = bt.box.extents();
-    const size_t nd = box.size();
-
-    // Drop unit outer dims, then merge dims contiguous for every ref.
-    std::vector<int64_t> ext;
-    std::vector<std::vector<int64_t>> st(refs.size());
-    for (size_t i = 0; i < nd; ++i) {
-      if (box[i] == 1 && i + 1 < nd) continue;  // the innermost (stride-1) dim always stays
-      ext.push_back(box[i]);
-      for (size_t k = 0; k < refs.size(); ++k) st[k].push_back(refs[k].st[i]);
-    }
-    for (int i = static_cast<int>(ext.size()) - 2; i >= 0; --i) {
-      bool merge = true;
-      for (size_t k = 0; k < refs.size(); ++k) merge = merge && st[k][i] == ext[i + 1] * st[k][i + 1];
-      if (!merge) continue;
-      ext[i] *= ext[i + 1];
-      ext.erase(ext.begin() + i + 1);
-      for (auto& s : st) {
-        s[i] = s[i + 1];
-        s.erase(s.begin() + i + 1);
-      }
-    }
-    if (ext.empty()) {
-      ext.push_back(1);
-      for (auto& s : st) s.push_back(1);
-    }
-    if (ext.size() > 4) fail(Errc::UnsupportedOp, "box needs more than 4 strided dims");
-    const int rd = static_cast<int>(ext.size());
-    for (int64_t e : ext)
+    const int rd = static_cast<int>(f.ext.size());
+    if (rd > 4) fail(Errc::UnsupportedOp, "box needs more than 4 strided dims");
+    for (int64_t e : f.ext)
       if (e > INT32_MAX) fail(Errc::UnsupportedOp, "box dim >= 2^31");
     TaskDesc td{};
-    for (int j = 0; j < 4; ++j) td.n[j] = j < rd ? static_cast<int32_t>(ext[rd - 1 - j]) : 1;
-
-    auto addr = [&](size_t k) {
-      return ctx_.arena_of(refs[k].L->rank) + refs[k].L->offset + refs[k].elem_off * es_;
-    };
-    auto ok = [&](int v) {
-      if ((static_cast<int64_t>(td.n[0]) * es_) % v) return false;
-      for (size_t k = 0; k < refs.size(); ++k) {
-        if (reinterpret_cast<uintptr_t>(addr(k)) % v) return false;
-        for (int j = 1; j < rd; ++j)
-          if ((st[k][rd - 1 - j] * es_) % v) return false;
-      }
-      return true;
-    };
-    int vb = 16;
-    while (vb > es_ && !ok(vb)) vb /= 2;
-    if (vb < es_) vb = es_;
+    for (int j = 0; j < 4; ++j) td.n[j] = j < rd ? static_cast<int32_t>(f.ext[rd - 1 - j]) : 1;
+    const int vb = f.vec_bytes;
     td.vec_bytes = vb;
     td.out0 = static_cast<int32_t>(H.terms.size());
     td.nout = static_cast<int32_t>(nout);
@@ -967,17 +1112,18 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     td.nterms = static_cast<int32_t>(bt.terms.size());
     td.ngroups = static_cast<int32_t>(bt.groups.size());
     for (size_t g = 0; g < bt.groups.size(); ++g) td.gsize[g] = static_cast<uint8_t>(bt.groups[g]);
-    bool all_local = true;
-    for (size_t k = 0; k < refs.size(); ++k) {
+    for (size_t k = 0; k < f.locs.size(); ++k) {
       TermDesc tm{};
-      tm.base = addr(k);
-      for (int j = 1; j < 4; ++j) tm.stride[j - 1] = j < rd ? st[k][rd - 1 - j] : 0;
+      tm.base = ctx_.arena_of(f.locs[k]->rank) + f.locs[k]->offset + f.elem_off[k] * es_;
+      for (int j = 1; j < 4; ++j) tm.stride[j - 1] = j < rd ? f.st[k][rd - 1 - j] : 0;
       H.terms.push_back(tm);
-      all_local = all_local && refs[k].L->rank == me;
     }
-    const bool tma = vb == 16 && (all_local || !(flags_ & HS_PROG_NO_TMA_PEER)) && !(flags_ & HS_PROG_NO_TMA);
+    const bool tma = tma_capable(bt);
+    if ((bt.wait >= 0 || !bt.targets.empty()) && !tma)
+      fail(Errc::UnsupportedOp, "streamed task is not TMA-capable");  // lower() checks first
     const int32_t task_id = static_cast<int32_t>(H.tasks.size());
     H.tasks.push_back(td);
+    H.src.push_back(&bt);
     stats_.tasks += 1;
     stats_.terms += td.nterms;
     stats_.outputs += td.nout;
@@ -1006,6 +1152,57 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     }
   }
 
+  // Streamed launches: signalling tasks' SigDescs and flag addresses; TMA
+  // items reordered into the two queues (signalling work first, then other
+  // non-waiting work; then waiting work), each by the piece's position along
+  // dim 0 so consumers follow their producers' progress.
+  std::vector<SigDesc> sigs;
+  std::vector<unsigned int*> targets;
+  std::vector<std::vector<int32_t>> task_sig(n_phases_);
+  std::vector<int32_t> n_first(n_phases_, 0);
+  std::vector<double> first_frac(n_phases_, 1.0);
+  for (int p = 0; p < n_phases_; ++p) {
+    Host& H = ph[p];
+    task_sig[p].assign(H.tasks.size(), -1);
+    if (!streamed_) {
+      n_first[p] = static_cast<int32_t>(H.items[0].size());
+      continue;
+    }
+    std::vector<int64_t> cnt(H.tasks.size(), 0);
+    for (const WorkItem& w : H.items[0]) cnt[w.task] += 1;
+    for (size_t k = 0; k < H.tasks.size(); ++k) {
+      const BoxTask& bt = *H.src[k];
+      if (bt.targets.empty() || cnt[k] == 0) continue;
+      task_sig[p][k] = static_cast<int32_t>(sigs.size());
+      sigs.push_back({static_cast<uint32_t>(sigs.size()), static_cast<uint32_t>(cnt[k]),
+                      static_cast<uint32_t>(targets.size()), static_cast<uint32_t>(bt.targets.size())});
+      for (const auto& [r, flag] : bt.targets)
+        targets.push_back(reinterpret_cast<unsigned int*>(ctx_.arena_of(r) + flag_off_) + flag);
+    }
+    auto rank_key = [&](const WorkItem& w) {
+      const BoxTask& bt = *H.src[w.task];
+      const int queue = bt.wait >= 0 ? 2 : bt.targets.empty() ? 1 : 0;
+      const double pos = static_cast<double>(bt.box.bounds[0][0]) / std::max<int64_t>(1, shapes_[bt.tensor][0]);
+      return std::make_pair(queue, pos);
+    };
+    std::stable_sort(H.items[0].begin(), H.items[0].end(),
+                     [&](const WorkItem& a, const WorkItem& b) { return rank_key(a) < rank_key(b); });
+    // CTAs of the first queue in proportion to its modelled time (HBM bytes
+    // at 6.5 TB/s vs NVLink bytes at 0.77 TB/s, whichever binds).
+    double hbm[2] = {0, 0}, nv[2] = {0, 0};
+    for (size_t k = 0; k < H.tasks.size(); ++k) {
+      const BoxTask& bt = *H.src[k];
+      const int q = bt.wait >= 0 ? 1 : 0;
+      const double bytes = static_cast<double>(bt.box.cells()) * es_;
+      for (const auto* ops : {&bt.dsts, &bt.terms})
+        for (const Operand& o : *ops) (loc(o.state, bt.tensor, o.dev).rank == bt.rank ? hbm : nv)[q] += bytes;
+    }
+    for (const WorkItem& w : H.items[0]) n_first[p] += H.src[w.task]->wait < 0 ? 1 : 0;
+    const double t0 = std::max(hbm[0] / 6.5e12, nv[0] / 7.7e11), t1 = std::max(hbm[1] / 6.5e12, nv[1] / 7.7e11);
+    first_frac[p] = t0 + t1 > 0 ? t0 / (t0 + t1) : 1.0;
+    if (const char* e = std::getenv("HS_STREAM_FIRST_FRAC")) first_frac[p] = std::atof(e);
+  }
+
   // TMA item records: header + every operand's first-row address, one
   // fixed-size slot per item so the producer warp never chases descriptors.
   std::vector<std::vector<uint4>> recs(n_phases_);
@@ -1021,6 +1218,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     for (size_t i = 0; i < H.items[0].size(); ++i) {
       const WorkItem& w = H.items[0][i];
       const TaskDesc& td = H.tasks[w.task];
+      const BoxTask& bt = *H.src[w.task];
       uint4* slot = recs[p].data() + i * W;
       TmaRecHead head{};
       head.nterms = td.nterms;
@@ -1028,6 +1226,9 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       head.ngroups = td.ngroups;
       head.nrow = w.nrow;
       head.nvcol = w.nvcol;
+      head.wait = bt.wait;
+      head.sig = task_sig[p][w.task];
+      head.need = bt.need;
       std::memcpy(head.gsize, td.gsize, sizeof(head.gsize));
       std::memcpy(slot, &head, sizeof(head));
       const int64_t i2 = w.plane % td.n[2], i3 = w.plane / td.n[2];
@@ -1061,8 +1262,11 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     offs[p].terms = reserve(ph[p].terms.size() * sizeof(TermDesc));
     for (int v = 0; v < kSlots; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
     offs[p].recs = reserve(recs[p].size() * sizeof(uint4));
-    offs[p].sched = reserve(2 * sizeof(int));  // zero-initialised scheduler words
+    offs[p].sched = reserve(4 * sizeof(int));  // zero-initialised scheduler words
   }
+  const size_t sigs_off = reserve(sigs.size() * sizeof(SigDesc));
+  const size_t targets_off = reserve(targets.size() * sizeof(unsigned int*));
+  const size_t done_off = reserve(sigs.size() * sizeof(unsigned long long));  // zero: no items done yet
   std::vector<char> host(std::max<size_t>(total, 1));
   for (int p = 0; p < n_phases_; ++p) {
     std::memcpy(host.data() + offs[p].tasks, ph[p].tasks.data(), ph[p].tasks.size() * sizeof(TaskDesc));
@@ -1072,6 +1276,8 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
                   ph[p].items[v].size() * sizeof(WorkItem));
     std::memcpy(host.data() + offs[p].recs, recs[p].data(), recs[p].size() * sizeof(uint4));
   }
+  std::memcpy(host.data() + sigs_off, sigs.data(), sigs.size() * sizeof(SigDesc));
+  std::memcpy(host.data() + targets_off, targets.data(), targets.size() * sizeof(unsigned int*));
   char* base = nullptr;
   if (!ctx_.is_analysis()) {
     cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
@@ -1090,24 +1296,50 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       n += cnt;
       if (!cnt) continue;
       Launch l;
-      l.tables = {reinterpret_cast<TaskDesc*>(base + offs[p].tasks),
-                  reinterpret_cast<TermDesc*>(base + offs[p].terms),
-                  reinterpret_cast<WorkItem*>(base + offs[p].items[v]),
-                  reinterpret_cast<const uint4*>(base + offs[p].recs),
-                  reinterpret_cast<int*>(base + offs[p].sched), cnt, rec_words[p], 0};
+      l.tables = PhaseTables{};
+      l.tables.tasks = reinterpret_cast<TaskDesc*>(base + offs[p].tasks);
+      l.tables.terms = reinterpret_cast<TermDesc*>(base + offs[p].terms);
+      l.tables.items = reinterpret_cast<WorkItem*>(base + offs[p].items[v]);
+      l.tables.recs = reinterpret_cast<const uint4*>(base + offs[p].recs);
+      l.tables.sched = reinterpret_cast<int*>(base + offs[p].sched);
+      l.tables.n_items = cnt;
+      l.tables.rec_words = rec_words[p];
       l.tma = v == 0;
       l.reduce = v >= 5;
       l.vec_bytes = v == 0 ? 16 : 16 >> ((v - 1) % 4);
       l.grid = l.tma ? std::max(1, std::min<int>(cnt, tma_grid(ctx_.sm_count())))
                      : std::max(1, std::min<int>(cnt, max_grid));
+      l.tables.n_first = cnt;
+      l.tables.first_ctas = l.grid;
+      l.tables.error = ctx_.error_flag();
+      if (l.tma && std::getenv("HS_TRACE") && !ctx_.is_analysis()) {
+        stats_.trace_off = ctx_.alloc(static_cast<size_t>(l.grid) * 64);
+        stats_.trace_ctas = l.grid;
+        l.tables.trace = reinterpret_cast<unsigned long long*>(ctx_.arena() + stats_.trace_off);
+      }
       if (l.tma) {
         stats_.tma_items += cnt;
-        // Single GPU: items are uniform local work, a static round-robin is
-        // best (no atomic on the producer's critical path).  Multi-GPU: local
-        // and NVLink items differ in cost, so the last ~1/16 are dynamic.
-        l.tables.n_static = ctx_.world() == 1
-                                ? cnt
-                                : static_cast<int32_t>((static_cast<int64_t>(cnt) * 15 / 16) / l.grid * l.grid);
+        if (streamed_) {
+          // two dynamic queues; no CTA takes a signalling item after a waiting one
+          l.tables.n_static = 0;
+          l.tables.n_first = n_first[p];
+          int fc = static_cast<int>(l.grid * first_frac[p] + 0.5);
+          if (n_first[p] == 0) fc = 0;
+          else if (n_first[p] == cnt) fc = l.grid;
+          else fc = std::min(l.grid - 1, std::max(1, fc));
+          l.tables.first_ctas = fc;
+          l.tables.sigs = reinterpret_cast<const SigDesc*>(base + sigs_off);
+          l.tables.targets = reinterpret_cast<unsigned int* const*>(base + targets_off);
+          l.tables.done = reinterpret_cast<unsigned long long*>(base + done_off);
+          l.tables.wait_flags = reinterpret_cast<const unsigned int*>(ctx_.arena() + flag_off_);
+        } else {
+          // Single GPU: items are uniform local work, a static round-robin is
+          // best (no atomic on the producer's critical path).  Multi-GPU: local
+          // and NVLink items differ in cost, so the last ~1/16 are dynamic.
+          l.tables.n_static = ctx_.world() == 1
+                                  ? cnt
+                                  : static_cast<int32_t>((static_cast<int64_t>(cnt) * 15 / 16) / l.grid * l.grid);
+        }
       }
       d.launches.push_back(l);
       ++launches;
@@ -1138,12 +1370,15 @@ void Program::run(cudaStream_t s) {
   // peers' destination shards ends with one more barrier, so a rank's own
   // destinations are complete when its stream is (callers still sync all
   // ranks before modifying sources).
+  ++runs_;
   for (int p = 0; p < n_phases_; ++p) {
     if (!nccl_mode_) ctx_.barrier(s);
     if (profiling_) event();
-    for (const Launch& l : dphases_[p].launches)
-      cuda_check(launch_phase(l.tables, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s),
-                 "box_phase launch");
+    for (const Launch& l : dphases_[p].launches) {
+      PhaseTables t = l.tables;
+      t.epoch = runs_;
+      cuda_check(launch_phase(t, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s), "box_phase launch");
+    }
     if (nccl_mode_ && p % 2 == 0 && !exchanges_[p / 2].empty()) {
       // the pack phase is followed by the phase's message exchange
       ncclComm_t comm = static_cast<ncclComm_t>(ctx_.nccl_comm());
@@ -1209,6 +1444,9 @@ std::string Program::tasks_json() const {
     ops(t.terms);
     o << ",\"groups\":[";
     for (size_t g = 0; g < t.groups.size(); ++g) o << (g ? "," : "") << t.groups[g];
+    o << "],\"wait\":" << t.wait << ",\"need\":" << t.need << ",\"targets\":[";
+    for (size_t g = 0; g < t.targets.size(); ++g)
+      o << (g ? "," : "") << "[" << t.targets[g].first << "," << t.targets[g].second << "]";
     o << "]}";
   }
   o << "]";
@@ -1228,7 +1466,9 @@ std::string Program::stats_json() const {
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes
-    << ",\"kernels_per_run\":" << stats_.kernels_per_run << ",\"phase_items\":[";
+    << ",\"kernels_per_run\":" << stats_.kernels_per_run << ",\"streamed\":" << (stats_.streamed ? 1 : 0)
+    << ",\"trace_off\":" << stats_.trace_off << ",\"trace_ctas\":" << stats_.trace_ctas
+    << ",\"phase_items\":[";
   for (size_t i = 0; i < stats_.phase_items.size(); ++i) o << (i ? "," : "") << stats_.phase_items[i];
   o << "],\"phase_bytes\":[";
   for (size_t i = 0; i < stats_.phase_bytes.size(); ++i)

@@ -52,6 +52,7 @@ class Context {
   void check_barrier_error();
 
   unsigned long long* scratch_counter() const { return counter_; }
+  int* error_flag() const { return barrier_error_; }
 
   // NCCL communicator over the same ranks (HS_PROG_NCCL baseline transport).
   void nccl_init(const unsigned char id[128]);
@@ -106,6 +107,10 @@ struct BoxTask {
   std::vector<Operand> dsts;    // >= 1; relay outputs may be on other ranks
   std::vector<Operand> terms;   // summation order; empty = zero-fill
   std::vector<int> groups;      // sizes; empty = flat (each term its own group)
+  // streamed programs (one launch for both plan phases):
+  int wait = -1;                // this consumer piece's flag index on its rank (-1: none)
+  int need = 0;                 // producer pieces that signal that flag per run
+  std::vector<std::pair<int, int>> targets;  // (rank, flag) signalled when this task is done
 };
 
 struct ProgramStats {
@@ -127,6 +132,9 @@ struct ProgramStats {
   int64_t dst_bytes = 0;     // destination-resident bytes on this rank
   int64_t src_bytes = 0;     // source-resident bytes on this rank
   int kernels_per_run = 0;   // phase kernels + barrier kernels
+  bool streamed = false;     // both plan phases in one launch (ready flags)
+  size_t trace_off = 0;      // EXPERIMENT
+  int trace_ctas = 0;
   std::vector<int64_t> phase_items;
   // per launched phase, this rank: {local HBM read, HBM write, NVLink in}
   std::vector<std::array<int64_t, 3>> phase_bytes;
@@ -166,13 +174,20 @@ class Program {
   };
 
   void lower(const CommPlan* comm, const SwitchPlan* sw);
-  enum class RelayMode { None, KeepLocal, FuseLocal };
+  // None: world 1 fusion.  KeepLocal / FuseLocal: remote mid reads become
+  // relays (producers store into the consumer's HBM).  Pull: remote mid
+  // reads pull the producer's materialised mid box (local groups fused).
+  enum class RelayMode { None, KeepLocal, FuseLocal, Pull };
   std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, RelayMode mode);
   double estimate_seconds(const std::vector<BoxTask>& tasks, int phases);
   void stage_for_nccl(std::vector<BoxTask>& tasks);
   void choose_replicas(std::vector<BoxTask>& tasks);
   std::vector<BoxTask> spread_shared(std::vector<BoxTask> tasks);
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
+  std::vector<BoxTask> stream_phases(const std::vector<BoxTask>& tasks);
+  struct Flat;
+  Flat flatten(const BoxTask& bt);
+  bool tma_capable(const BoxTask& bt);
   void build_tables(const std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);
 
@@ -193,6 +208,9 @@ class Program {
   void* dev_block_ = nullptr;
   bool profiling_ = false;
   bool remote_final_writes_ = false;  // last phase stores into peers' shards
+  bool streamed_ = false;             // both plan phases in one launch (ready flags)
+  size_t flag_off_ = 0;               // arena offset of the symmetric ready-flag array
+  uint32_t runs_ = 0;                 // run counter = flag epoch
   // HS_PROG_NCCL baseline: per plan phase, this rank's grouped send/recv list
   struct Exchange {
     int peer;

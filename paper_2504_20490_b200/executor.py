@@ -37,6 +37,8 @@ HS_PROG_PULL_COPIES = 256  # world > 1: copies pull (run on the destination's ra
 HS_PROG_RELAY_KEEP_LOCAL = 512  # world > 1: relay-waiting tasks keep local groups before the barrier
 HS_PROG_PUSH_ALL = 1024    # world > 1: every copy runs on its input's rank (before output merging)
 HS_PROG_NCCL = 2048         # world > 1: NCCL grouped send/recv transport (baseline)
+HS_PROG_NO_STREAM = 4096    # world > 1: barrier between plan phases (no per-chunk ready flags)
+HS_PROG_PULL_MID = 8192     # world > 1: pull remote mid boxes (no relay stores), local groups fused
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -290,7 +292,8 @@ class Program:
 
 
 AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES,
-                       HS_PROG_PUSH_ALL, HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE, HS_PROG_RELAY_KEEP_LOCAL]
+                       HS_PROG_PUSH_ALL, HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE, HS_PROG_RELAY_KEEP_LOCAL,
+                       HS_PROG_NO_STREAM, HS_PROG_PULL_MID | HS_PROG_NO_STREAM]
 
 
 def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps: int = 5,
@@ -312,7 +315,8 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
     best, best_ms, timings = None, None, {}
     for flags in cands:
         prog = Program(ctx, plan, layout, flags)
-        if flags & HS_PROG_RELAY_KEEP_LOCAL and prog.stats()["plan_phases"] < 2:
+        two_phase_only = HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_PULL_MID
+        if flags & two_phase_only and prog.stats()["plan_phases"] < 2:  # same program as another candidate
             prog.close()
             continue
         for _ in range(2):

@@ -39,10 +39,19 @@ def main():
         nonlocal ok
         mark = ctx.alloc(0)
         lay = ShardLayout(ctx, plan, n_virtual)
-        lay.fill_src(11, mode)
         for flags in flag_sets:
-            lay.clear_dst()
+            # run 1 on other values, run 2 (flag epoch 2) on the checked ones:
+            # a consumer that does not wait for this run's producers reads
+            # run 1's relays and fails the comparison
+            lay.fill_src(12, mode)
             prog = Program(ctx, plan, lay, flags)
+            prog.run()
+            ctx.sync()
+            dist.barrier()
+            lay.fill_src(11, mode)
+            lay.clear_dst()
+            ctx.sync()
+            dist.barrier()
             prog.run()
             ctx.sync()
             want = src_of()
@@ -53,7 +62,8 @@ def main():
                     bad.append(dev)
             st = prog.stats()
             results.append({"case": name, "flags": flags, "bad": bad, "nvlink_in": st["nvlink_in"],
-                            "nvlink_out": st["nvlink_out"], "hbm_write": st["hbm_write"]})
+                            "nvlink_out": st["nvlink_out"], "hbm_write": st["hbm_write"],
+                            "streamed": st.get("streamed", 0), "tasks": st["tasks"]})
             ok = ok and not bad
             prog.close()
             dist.barrier()

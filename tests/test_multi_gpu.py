@@ -26,14 +26,20 @@ def _gpus():
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("flags", ["0,14,1", "16,17,32,48", "128,256,480", "512,1024,1152", "2048,2062"])  # see HS_PROG_*
+# flag sets (HS_PROG_*); "fine:" = streamed programs cut into ~1 KB chunks so
+# the small cases exercise many ready flags per run
+@pytest.mark.parametrize("flags", ["0,14,1", "16,17,32,48", "128,256,480", "512,1024,1152", "2048,2062",
+                                   "4096,4128,8192,12288", "fine:0,32,512,1024,8192"])
 def test_multi_gpu_parity(tmp_path, flags):
     n = min(_gpus(), 8)
+    port = 29517 + sum(map(ord, flags)) % 300
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29517 + len(flags)}",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
     out = os.path.join(tmp_path, "mgpu")
-    env = dict(os.environ, HS_MGPU_OUT=out, HS_MGPU_FLAGS=flags)
+    env = dict(os.environ, HS_MGPU_OUT=out, HS_MGPU_FLAGS=flags.removeprefix("fine:"))
+    if flags.startswith("fine:"):
+        env["HS_STREAM_CHUNK_KB"] = "1"
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = []

@@ -22,7 +22,8 @@ from paper_2504_20490_b200 import workloads as W
 from paper_2504_20490_b200.executor import analyze
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-FLAG_SETS = [0, 14, 1, 32, 128, 256, 512, 1024, 1152, 2048, 2062]
+FLAG_SETS = [0, 14, 1, 32, 128, 256, 512, 1024, 1152, 2048, 2062, 4096, 8192, 12288]
+HEAVY = {"cfg3a", "cfg3c"}  # thousands of streamed pieces: default and unstreamed only
 NAMES = ["cfg1A", "cfg1B", "cfg1C", "cfg1D", "cfg2e", "cfg2a", "cfg2b", "cfg2d", "cfg3b", "cfg3a",
          "cfg3c", "cfg4"]
 
@@ -72,22 +73,39 @@ def check_partition(w, plan, per_rank, world):
                 produced.setdefault((kind, t["tensor"], dev, rank), []).append((t["phase"], t["box"]))
             if kind == "send":  # NCCL staging slot: one index space across ranks
                 produced.setdefault(("recv", t["tensor"], dev), []).append((t["phase"], t["box"], rank))
+    signallers = {}
     for t in tasks:
+        for r, f in t.get("targets", []):
+            signallers.setdefault((r, f), []).append(t)
+    streamed = any(s.get("streamed") for s in stats)
+    for t in tasks:
+        if t.get("wait", -1) >= 0:
+            assert len(signallers.get((t["rank"], t["wait"]), [])) == t["need"], t
         for kind, dev, rank in t["terms"]:
             if kind == "relay":
                 assert rank == t["rank"], t
-            if kind in ("relay", "mid", "recv"):
+            if kind in ("relay", "mid") and streamed:
+                # one launch: the pieces that signal this task's flag must cover what it reads
+                assert t["wait"] >= 0, t
+                cover = [p["box"] for p in signallers[(t["rank"], t["wait"])]
+                         if any(o[0] == kind and o[1] == dev for o in p["dsts"])]
+            elif kind in ("relay", "mid", "recv"):
                 if kind == "recv":
                     cover = [b for ph, b, r in produced.get((kind, t["tensor"], dev), [])
                              if ph < t["phase"] and r != t["rank"]]
                 else:
                     cover = [b for ph, b in produced.get((kind, t["tensor"], dev, rank), []) if ph < t["phase"]]
+            if kind in ("relay", "mid", "recv"):
                 inside = [[[max(lo, a), min(hi, b)] for (lo, hi), (a, b) in zip(c, t["box"])] for c in cover
                           if all(max(lo, a) < min(hi, b) for (lo, hi), (a, b) in zip(c, t["box"]))]
                 assert _boxes_tile(t["box"], inside), (w.name, t)
         for kind, dev, rank in t["dsts"]:
             if rank != t["rank"]:
                 assert kind in ("relay", "dst", "mid"), t
+
+
+def flag_sets(name):
+    return [0, 4096, 8192] if name in HEAVY else FLAG_SETS
 
 
 def _analyze_all(w, plan, world, flags):
@@ -99,7 +117,7 @@ def test_partitioning_in_process(world):
     for name in NAMES:
         w = W.by_name(name)
         plan = _plan(w)
-        for flags in FLAG_SETS:
+        for flags in flag_sets(name):
             check_partition(w, plan, _analyze_all(w, plan, world, flags), world)
 
 
@@ -112,13 +130,13 @@ sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r}
 import torch.distributed as dist
 from paper_2504_20490_b200 import workloads as W
 from paper_2504_20490_b200.executor import analyze
-from test_multirank_cpu import NAMES, FLAG_SETS, _plan, check_partition
+from test_multirank_cpu import NAMES, flag_sets, _plan, check_partition
 dist.init_process_group('gloo')
 rank, world = dist.get_rank(), dist.get_world_size()
 ok = True
 for name in NAMES:
     w = W.by_name(name); plan = _plan(w)
-    for flags in FLAG_SETS:
+    for flags in flag_sets(name):
         mine = analyze(plan, world, rank, w.n_virtual, flags)
         allr = [None] * world
         dist.all_gather_object(allr, mine)
