@@ -130,6 +130,9 @@ enum {
                                      producer's HBM (local groups still fused) instead of
                                      relay stores into the consumer's HBM */
 };
+/* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
+ * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */
+#define HS_PROG_STREAM_SHARE(sixty_fourths) (((sixty_fourths) & 0xff) << 16)
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);
 void hs_prog_destroy(hs_prog* prog);

@@ -589,6 +589,125 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
   if (lane == 0) atomicAdd(&ring->consumers_done, 1u);
 }
 
+// ---- multi-GPU launches without ready flags: static round-robin for ~15/16
+// of the items, then one atomic per item (the kernel measured before the
+// streamed variant existed; kept verbatim -- the streamed kernel's extra warp
+// and ticket logic cost ~5% on copy-heavy plans).
+// One consumer-warp pass over pipeline stage `iter`: wait for it, form every
+// output vector of the item from shared memory, release the stage.  Returns
+// false on the producer's end marker.
+template <class T>
+__device__ __forceinline__ bool tma_consume_tail(const unsigned char* stage, const uint4* meta,
+                                            uint64_t* full, uint64_t* empty, int iter, int lane) {
+  const int ctid = threadIdx.x - 32;
+  constexpr int nct = kTmaThreads - 32;
+  const int s = iter % kTmaStages;
+  mbar_wait(&full[s], (iter / kTmaStages) & 1);
+  const uint4* m = meta + s * 32;
+  const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
+  const int nt = h->nterms;
+  if (nt < 0) return false;
+  const int nvcol = h->nvcol, nvec = h->nrow * h->nvcol, no = h->nout;
+  const int ng = h->ngroups;
+  const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;
+  const unsigned char* in = stage + s * kStageBytes;
+  for (int v = ctid; v < nvec; v += nct) {
+    const int r = v / nvcol;
+    const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
+    uint4 val;
+    if (nt == 0) {
+      val = make_uint4(0, 0, 0, 0);
+    } else if (nt == 1) {
+      val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
+    } else {
+      val = grouped_sum<T, 16>(nt, ng, h->gsize, [&](int k) {
+        return *reinterpret_cast<const uint4*>(in + (static_cast<size_t>(k) * nvec + v) * 16);
+      });
+    }
+    for (int o = 0; o < no; ++o) __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[s]);
+  return true;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(PhaseTables t) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* stage = smem;
+  uint4* meta = reinterpret_cast<uint4*>(smem + kTmaStages * kStageBytes);  // 32 words per stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kTmaStages * 32);
+  uint64_t* empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int W = t.rec_words;
+
+  if (warp == 0) {
+    // ---- producer warp: the item record is prefetched one item ahead (one
+    // 16-byte word per lane); lane k then streams term k's rows.
+    // Items [0, n_static) are dealt round-robin (no dependency: the record is
+    // prefetched one item ahead); the tail is handed out dynamically (one
+    // atomic per item) so CTAs that drew cheap items keep pulling work.
+    const unsigned full_mask = 0xffffffffu;
+    auto next_item = [&](int prev, int iter_next) {
+      const int st = blockIdx.x + iter_next * static_cast<int>(gridDim.x);
+      if (st < t.n_static) return st;
+      int d = lane == 0 ? atomicAdd(&t.sched[0], 1) : 0;
+      return t.n_static + __shfl_sync(full_mask, d, 0);
+    };
+    int it = next_item(-1, 0);
+    uint4 next = make_uint4(0, 0, 0, 0);
+    if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+    for (int iter = 0;; ++iter) {
+      const int cur_it = it;
+      const uint4 cur = next;
+      if (cur_it < t.n_items) {
+        const int nxt = next_item(cur_it, iter + 1);
+        it = nxt;
+        if (nxt < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nxt) * W + lane];
+      }
+      const int s = iter % kTmaStages;
+      if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
+      uint4* m = meta + s * 32;
+      if (cur_it >= t.n_items) {  // end marker for the consumers
+        if (lane == 0) {
+          reinterpret_cast<TmaRecHead*>(m)->nterms = -1;
+          mbar_arrive_expect_tx(&full[s], 0);
+          // the last CTA out resets the scheduler for the next launch
+          if (atomicAdd(&t.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+            t.sched[0] = 0;
+            t.sched[1] = 0;
+          }
+        }
+        return;
+      }
+      if (lane < W) m[lane] = cur;
+      __syncwarp();
+      const TmaRecHead* h = reinterpret_cast<const TmaRecHead*>(m);
+      const int nt = h->nterms, nrow = h->nrow;
+      const uint32_t row_bytes = static_cast<uint32_t>(h->nvcol) * 16;
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], row_bytes * nrow * nt);  // release: meta
+      __syncwarp();
+      if (lane < nt) {
+        const TmaOperand op = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords)[lane];
+        unsigned char* dst = stage + s * kStageBytes + static_cast<size_t>(lane) * nrow * row_bytes;
+        for (int r = 0; r < nrow; ++r) bulk_g2s(dst + r * row_bytes, op.row0 + r * op.step, row_bytes, &full[s]);
+      }
+    }
+  }
+
+  // ---- consumers (until the producer's end marker)
+  for (int iter = 0;; ++iter)
+    if (!tma_consume_tail<T>(stage, meta, full, empty, iter, lane)) break;
+}
+
 // Single-GPU variant (items dealt round-robin, no scheduler state): the
 // kernel measured at 93% of HBM peak on cfg2e; kept verbatim because the
 // dynamic-schedule kernel's extra per-item work costs ~8% there.
@@ -853,13 +972,17 @@ struct PhaseK {
                              static_cast<int>(kDynSmem));
         cudaFuncSetAttribute(box_phase_tma_static_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kTmaSmem));
+        cudaFuncSetAttribute(box_phase_tma_tail_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kTmaSmem));
         return true;
       }();
       (void)configured;
-      if (t.n_static >= t.n_items)
+      if (t.sigs)  // streamed: ready flags, two queues, signaller warp
+        box_phase_tma_kernel<T><<<g, dim3(kDynThreads), kDynSmem, s>>>(t);
+      else if (t.n_static >= t.n_items)
         box_phase_tma_static_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       else
-        box_phase_tma_kernel<T><<<g, dim3(kDynThreads), kDynSmem, s>>>(t);
+        box_phase_tma_tail_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       return;
     }
     if (reduce)
