@@ -7,6 +7,9 @@
 // in hshard/exec.hpp.
 #pragma once
 
+#include <map>
+#include <string>
+
 #include "hshard/bsr.hpp"
 
 namespace hshard {
@@ -19,8 +22,8 @@ struct SwitchEntry {
   Shape shape;
 };
 
-// A parameter's layout under two strategies (the CompGraph that would supply
-// these per-strategy slots is outside the resharding path).
+// A parameter's layout under two strategies (a CompGraph's slots supply them
+// through the overload below).
 struct ParamLayouts {
   int tensor_id = 0;
   Shape shape;
@@ -30,6 +33,13 @@ struct ParamLayouts {
 
 // Changed parameters only; annotations_equal pairs are omitted.
 std::vector<SwitchEntry> diff_strategies(const std::vector<ParamLayouts>& params);
+
+class CompGraph;
+// SPEC.md:413-418 as specified: the Parameters of a deduced graph whose
+// annotation differs between strategies a and b, shapes bound with
+// `bindings` (graph.hpp).  UndeducedStrategy if a slot is empty.
+std::vector<SwitchEntry> diff_strategies(const CompGraph& graph, int a, int b,
+                                         const std::map<std::string, int64_t>& bindings = {});
 
 struct SwitchPlan {
   std::vector<SwitchEntry> diff;  // tensor order of the plan

@@ -74,6 +74,19 @@ int hs_validate(const char* anno, const int64_t* shape, int ndim, char** json);
  *                                                  reference annotation.hpp:143 */
 int hs_align_shard_specs(const char* a, const char* b, char** json);
 
+/* ---------------------------------------------------------------- strategy source
+ * CompGraph + deduce_graph (reference graph.hpp:105-141, deduction.hpp:29-31)
+ * and diff_strategies(graph, a, b).  `graph` is the line
+ * form parsed by hshard::parse_graph (include/hshard/graph.hpp).
+ * hs_graph_deduce deduces every strategy independently -> JSON
+ *   {"tensors":[{"id","name","kind","shape","dtype","producer"}...],
+ *    "topo":[node ids], "symbols":[...],
+ *    "strategies":[{"ok":1,"slots":[anno or null...]} | {"ok":0,"error":Errc,"message":...}]}
+ * hs_graph_diff deduces strategies a and b, binds symbols from `bindings`
+ * ("B=8,S=2048"; NULL = none) -> JSON [{"tensor","name","src","dst","shape"}...]. */
+int hs_graph_deduce(const char* graph, char** json);
+int hs_graph_diff(const char* graph, int a, int b, const char* bindings, char** json);
+
 /* ---------------------------------------------------------------- executor
  * The reference declares execute_plan (sim.hpp:77-79) but never defines it;
  * this is its B200 implementation.  One hs_ctx per process; one process per

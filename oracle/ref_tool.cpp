@@ -40,6 +40,8 @@
 #include <vector>
 
 #include "hshard/bsr.hpp"
+#include "hshard/deduction.hpp"
+#include "hshard/graph.hpp"
 #include "hshard/resolve.hpp"
 #include "hshard/tensor.hpp"
 
@@ -535,6 +537,70 @@ std::string cmd_execute(const std::vector<std::string>& f) {
   return o;
 }
 
+// G|stmt&stmt&...: build the reference CompGraph from the line form of
+// include/hshard/graph.hpp (parse_graph), deduce every strategy with the
+// reference deduce_graph (deduction.cpp:318-353), print the slots.
+std::string cmd_graph(const std::string& program) {
+  CompGraph g;
+  bool first = true;
+  for (const std::string& raw : split(program, '&')) {
+    const std::string st = trim(raw);
+    if (st.empty()) continue;
+    std::istringstream is(st);
+    std::vector<std::string> w;
+    for (std::string x; is >> x;) w.push_back(x);
+    auto shape_from = [&](size_t k) {
+      SymShape sh;
+      for (size_t i = k; i < w.size(); ++i) sh.push_back(SymDim::parse(w[i]));
+      return sh;
+    };
+    const std::string& op = w[0];
+    if (op == "strategies") {
+      if (!first) throw std::runtime_error("strategies must come first");
+      for (int k = 1; k < std::stoi(w.at(1)); ++k) g.add_strategy();
+    } else if (op == "placeholder") {
+      g.placeholder(w.at(1), shape_from(3), parse_dtype(w.at(2)));
+    } else if (op == "parameter") {
+      g.parameter(w.at(1), shape_from(3), parse_dtype(w.at(2)));
+    } else if (op == "elementwise") {
+      g.elementwise(ew_func_from_name(w.at(1)), std::stoi(w.at(2)));
+    } else if (op == "dot") {
+      g.dot(std::stoi(w.at(1)), std::stoi(w.at(2)));
+    } else if (op == "sum") {
+      g.sum(std::stoi(w.at(1)), std::stoi(w.at(2)));
+    } else if (op == "reshape") {
+      g.reshape(std::stoi(w.at(1)), shape_from(2));
+    } else if (op == "comm") {
+      g.comm(std::stoi(w.at(1)), w.at(2) == "auto" ? std::nullopt : std::optional<bool>(w.at(2) == "1"));
+    } else if (op == "annotate") {
+      // annotation text = everything after the third word
+      size_t pos = 0;
+      for (int k = 0; k < 3; ++k) {
+        pos = st.find_first_not_of(" ", pos);
+        pos = st.find(' ', pos);
+      }
+      g.set_annotation(std::stoi(w.at(1)), std::stoi(w.at(2)), parse_anno(st.substr(pos)));
+    } else {
+      throw std::runtime_error("unknown statement " + op);
+    }
+    first = false;
+  }
+  std::string o = "{\"topo\":" + jints(g.topo_order()) + ",\"strategies\":[";
+  for (int s = 0; s < g.strategy_count(); ++s) {
+    if (s) o += ",";
+    try {
+      deduce_graph(g, s);
+      o += "{\"ok\":1,\"slots\":[";
+      for (const auto& t : g.tensors())
+        o += std::string(t.id ? "," : "") + (t.slots.at(s) ? jstr(t.slots.at(s)->str()) : "null");
+      o += "]}";
+    } catch (const Error& e) {
+      o += "{\"ok\":0,\"error\":" + jstr(errc_name(e.code())) + "}";
+    }
+  }
+  return o + "]}";
+}
+
 std::string handle(const std::string& line, std::istream& in) {
   auto f = split(line, '|');
   const std::string& c = f.at(0);
@@ -604,6 +670,7 @@ std::string handle(const std::string& line, std::istream& in) {
     return o + "]";
   }
   if (c == "X") return cmd_execute(f);
+  if (c == "G") return cmd_graph(line.substr(2));
   return "{\"error\":\"UnknownCommand\"}";
 }
 

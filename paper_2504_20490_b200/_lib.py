@@ -57,6 +57,9 @@ def _load() -> ctypes.CDLL:
         "hs_annotations_equal": (c_int, [c_char_p, c_char_p, P(c_int)]),
         "hs_validate": (c_int, [c_char_p, P(c_int64), c_int, P(c_void_p)]),
         "hs_align_shard_specs": (c_int, [c_char_p, c_char_p, P(c_void_p)]),
+        # strategy source
+        "hs_graph_deduce": (c_int, [c_char_p, P(c_void_p)]),
+        "hs_graph_diff": (c_int, [c_char_p, c_int, c_int, c_char_p, P(c_void_p)]),
         # executor
         "hs_ctx_create": (c_int, [c_int, c_int, c_int, c_size_t, P(c_void_p)]),
         "hs_ctx_destroy": (None, [c_void_p]),

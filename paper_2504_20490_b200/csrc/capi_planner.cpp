@@ -1,9 +1,13 @@
 // hshard-b200 C ABI: planner entry points (include/hshard_c.h).
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <sstream>
 #include <variant>
 
 #include "capi_common.hpp"
+#include "hshard/deduction.hpp"
+#include "hshard/graph.hpp"
 #include "hshard/resolve.hpp"
 #include "hshard/switch.hpp"
 
@@ -146,6 +150,89 @@ int hs_align_shard_specs(const char* a, const char* b, char** json) {
       s += std::string(i ? "," : "") + "[" + std::to_string((*f)[i].key_a) + "," +
            std::to_string((*f)[i].key_b) + "," + std::to_string((*f)[i].count) + "]";
     *json = dup_string(s + "]");
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- strategy source
+namespace {
+
+std::string quoted(const std::string& v) {
+  std::string o = "\"";
+  for (char c : v) {
+    if (c == '"' || c == '\\') o += '\\';
+    o += c;
+  }
+  return o + "\"";
+}
+
+std::map<std::string, int64_t> parse_bindings(const char* text) {
+  std::map<std::string, int64_t> b;
+  if (!text) return b;
+  std::stringstream ss(text);
+  for (std::string item; std::getline(ss, item, ',');) {
+    if (item.find_first_not_of(' ') == std::string::npos) continue;
+    const auto eq = item.find('=');
+    if (eq == std::string::npos) fail(Errc::ParseError, "binding '" + item + "' lacks '='");
+    std::string k = item.substr(0, eq);
+    k.erase(0, k.find_first_not_of(' '));
+    k.erase(k.find_last_not_of(' ') + 1);
+    b[k] = std::stoll(item.substr(eq + 1));
+  }
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hs_graph_deduce(const char* graph, char** json) {
+  return capi::guarded([&] {
+    CompGraph g = parse_graph(graph);
+    std::string o = "{\"tensors\":[";
+    for (const TensorRef& t : g.tensors())
+      o += std::string(t.id ? "," : "") + "{\"id\":" + std::to_string(t.id) + ",\"name\":" + quoted(t.name) +
+           ",\"kind\":" + quoted(op_kind_name(g.node(t.producer).kind)) + ",\"shape\":" +
+           quoted(sym_shape_str(t.shape)) + ",\"dtype\":" + quoted(dtype_name(t.dtype)) +
+           ",\"producer\":" + std::to_string(t.producer) + "}";
+    o += "],\"topo\":[";
+    const auto order = g.topo_order();
+    for (size_t i = 0; i < order.size(); ++i) o += (i ? "," : "") + std::to_string(order[i]);
+    o += "],\"symbols\":[";
+    const auto syms = g.symbols();
+    for (size_t i = 0; i < syms.size(); ++i) o += (i ? "," : "") + quoted(syms[i]);
+    o += "],\"strategies\":[";
+    for (int s = 0; s < g.strategy_count(); ++s) {
+      o += s ? "," : "";
+      try {
+        deduce_graph(g, s);
+        o += "{\"ok\":1,\"slots\":[";
+        for (const TensorRef& t : g.tensors())
+          o += std::string(t.id ? "," : "") + (t.slots.at(s) ? quoted(t.slots.at(s)->str()) : "null");
+        o += "]}";
+      } catch (const Error& e) {
+        o += "{\"ok\":0,\"error\":" + quoted(errc_name(e.code())) + ",\"message\":" + quoted(e.what()) + "}";
+      }
+    }
+    *json = capi::dup_string(o + "]}");
+  });
+}
+
+int hs_graph_diff(const char* graph, int a, int b, const char* bindings, char** json) {
+  return capi::guarded([&] {
+    CompGraph g = parse_graph(graph);
+    deduce_graph(g, a);
+    if (b != a) deduce_graph(g, b);
+    const auto diff = diff_strategies(g, a, b, parse_bindings(bindings));
+    std::string o = "[";
+    for (size_t i = 0; i < diff.size(); ++i) {
+      const SwitchEntry& e = diff[i];
+      o += std::string(i ? "," : "") + "{\"tensor\":" + std::to_string(e.tensor_id) + ",\"name\":" +
+           quoted(g.tensor(e.tensor_id).name) + ",\"src\":" + quoted(e.src.str()) + ",\"dst\":" +
+           quoted(e.dst.str()) + ",\"shape\":[" + join_ints(e.shape) + "]}";
+    }
+    *json = capi::dup_string(o + "]");
   });
 }
 

@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <string>
 
+#include "hshard/deduction.hpp"
+#include "hshard/graph.hpp"
 #include "hshard/resolve.hpp"
 #include "hshard/sim.hpp"
 #include "hshard/switch.hpp"
@@ -25,6 +27,10 @@ static Tensor iota(Shape s, DType dt, double scale = 1.0) {
   Tensor t(s, dt);
   for (size_t i = 0; i < t.data.size(); ++i) t.data[i] = static_cast<double>((i * 7) % 13) * scale - 5;
   return t;
+}
+
+static bool comm_kind_ok(const CompGraph& g, int node) {
+  return g.node(node).kind == OpKind::CommOp && !g.comm_once(node);  // fed by a placeholder path
 }
 
 static void cpu_tests() {
@@ -77,6 +83,30 @@ static void cpu_tests() {
   int64_t unfused = 0;
   for (const auto& e : diff) unfused += make_plan(build_table(e.src, e.dst, e.shape, e.tensor_id, 2), Bandwidth::uniform()).total_bytes();
   CHECK(sp.plan.total_bytes() == unfused);
+
+  // strategy source, as a reference user builds it (graph.hpp / deduction.hpp):
+  // Megatron MLP under TP2 and TP4, deduced, then diffed into switch entries
+  CompGraph g;
+  const int s1 = g.add_strategy();
+  const int gx = g.placeholder("x", {SymDim::sym("B"), SymDim::lit(64)}, DType::F32);
+  const int w1 = g.parameter("w1", {SymDim::lit(64), SymDim::lit(256)}, DType::F32);
+  const int h = g.elementwise(EwFunc::Gelu, g.dot(gx, w1));
+  const int w2 = g.parameter("w2", {SymDim::lit(256), SymDim::lit(64)}, DType::F32);
+  const int y = g.comm(g.dot(h, w2));
+  const DeviceGroup t2({0, 1});
+  for (int s : {0, s1}) {
+    const DeviceGroup& tg = s == 0 ? t2 : g4;
+    const int n = tg.size();
+    g.set_annotation(gx, s, HetAnnotation::single(tg, {{kDuplicate, n}}));
+    g.set_annotation(w1, s, HetAnnotation::single(tg, {{1, n}}));
+    g.set_annotation(w2, s, HetAnnotation::single(tg, {{0, n}}));
+    g.set_annotation(y, s, HetAnnotation::single(tg, {{kDuplicate, n}}));
+    deduce_graph(g, s);
+  }
+  CHECK(g.tensor(g.node(y).inputs[0]).slots[0]->ds_union[0].count_of(kPartial) == 2);  // row-parallel
+  const auto moves = diff_strategies(g, 0, s1, {{"B", 8}});
+  CHECK(moves.size() == 2 && moves[0].shape == Shape({64, 256}));
+  CHECK(comm_kind_ok(g, y));
 }
 
 static void gpu_tests() {

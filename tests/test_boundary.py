@@ -40,7 +40,8 @@ def test_cpp_api_symbols_exported():
                 "hshard::placement(", "hshard::convert_hsize(", "hshard::bottom_resolve(",
                 "hshard::top_resolve(", "hshard::execute_plan(", "hshard::apply_switch(",
                 "hshard::plan_switch(", "hshard::reassemble(", "hshard::scatter(",
-                "hshard::volume_report(", "hshard::Tensor::slice("]:
+                "hshard::volume_report(", "hshard::Tensor::slice(", "hshard::deduce_graph(",
+                "hshard::CompGraph::dot(", "hshard::unify_inputs(", "hshard::diff_strategies(hshard::CompGraph"]:
         assert sym in out, sym
 
 
