@@ -301,7 +301,7 @@ def HS_PROG_STREAM_SHARE(sixty_fourths: int) -> int:
 AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES,
                        HS_PROG_PUSH_ALL, HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE, HS_PROG_RELAY_KEEP_LOCAL,
                        HS_PROG_NO_STREAM, HS_PROG_PULL_MID | HS_PROG_NO_STREAM,
-                       HS_PROG_STREAM_SHARE(32), HS_PROG_STREAM_SHARE(51)]
+                       HS_PROG_STREAM_SHARE(32), HS_PROG_STREAM_SHARE(51), HS_PROG_FUSE_PHASES]
 
 
 def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps: int = 5,
@@ -323,7 +323,8 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
     best, best_ms, timings = None, None, {}
     for flags in cands:
         prog = Program(ctx, plan, layout, flags)
-        two_phase_only = HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_PULL_MID | HS_PROG_STREAM_SHARE(0xFF)
+        two_phase_only = (HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_PULL_MID | HS_PROG_STREAM_SHARE(0xFF)
+                          | HS_PROG_FUSE_PHASES)
         if flags & two_phase_only and prog.stats()["plan_phases"] < 2:  # same program as another candidate
             prog.close()
             continue
