@@ -35,10 +35,12 @@ class Graph:
         self._lines = [f"strategies {strategies}"]
         self._n = 0
         self.names: Dict[str, int] = {}
+        self.nodes: List[dict] = []  # graph JSON v1 node records (formats.graph_to_json)
 
     # ---- builders (each returns the new node / tensor id)
-    def _add(self, stmt: str) -> int:
+    def _add(self, stmt: str, **node) -> int:
         self._lines.append(stmt)
+        self.nodes.append({"id": self._n, **node, "annotations": {}})
         self._n += 1
         return self._n - 1
 
@@ -48,31 +50,36 @@ class Graph:
 
     def placeholder(self, name: str, shape: Sequence[Dim], dtype: str = "f64") -> int:
         self.names[name] = self._n
-        return self._add(f"placeholder {name} {dtype} {self._dims(shape)}")
+        return self._add(f"placeholder {name} {dtype} {self._dims(shape)}", kind="Placeholder", name=name,
+                         shape=[str(d) for d in shape], dtype=dtype)
 
     def parameter(self, name: str, shape: Sequence[Dim], dtype: str = "f64") -> int:
         self.names[name] = self._n
-        return self._add(f"parameter {name} {dtype} {self._dims(shape)}")
+        return self._add(f"parameter {name} {dtype} {self._dims(shape)}", kind="Parameter", name=name,
+                         shape=[str(d) for d in shape], dtype=dtype)
 
     def elementwise(self, func: str, x: int) -> int:
-        return self._add(f"elementwise {func} {x}")
+        return self._add(f"elementwise {func} {x}", kind="Elementwise", inputs=[x], func=func)
 
     def dot(self, x: int, w: int) -> int:
-        return self._add(f"dot {x} {w}")
+        return self._add(f"dot {x} {w}", kind="Dot", inputs=[x, w])
 
     def sum(self, x: int, axis: int) -> int:
-        return self._add(f"sum {x} {axis}")
+        return self._add(f"sum {x} {axis}", kind="Sum", inputs=[x], axis=axis)
 
     def reshape(self, x: int, shape: Sequence[Dim]) -> int:
-        return self._add(f"reshape {x} {self._dims(shape)}")
+        return self._add(f"reshape {x} {self._dims(shape)}", kind="Reshape", inputs=[x],
+                         target=[str(d) for d in shape])
 
     def comm(self, x: int, once: Optional[bool] = None) -> int:
-        return self._add(f"comm {x} {'auto' if once is None else int(bool(once))}")
+        return self._add(f"comm {x} {'auto' if once is None else int(bool(once))}", kind="CommOp", inputs=[x],
+                         once=once)
 
     def annotate(self, node: int, strategy: int, anno: str) -> None:
         if not 0 <= strategy < self.strategies:
             raise ValueError(f"strategy {strategy} out of range")
         self._lines.append(f"annotate {node} {strategy} {anno}")
+        self.nodes[node]["annotations"][str(strategy)] = anno
 
     # ---- queries
     def text(self) -> str:
