@@ -86,6 +86,12 @@ int hs_align_shard_specs(const char* a, const char* b, char** json);
  * ("B=8,S=2048"; NULL = none) -> JSON [{"tensor","name","src","dst","shape"}...]. */
 int hs_graph_deduce(const char* graph, char** json);
 int hs_graph_diff(const char* graph, int a, int b, const char* bindings, char** json);
+/* Executable-graph specialization (reference specialize.hpp:27-85): deduce
+ * `strategy`, then -> JSON {"phases": {node: "prologue"|"body"|"epilogue"},
+ *   "exec_graphs": [{"device", "nodes": [{"node", "comm", "phase", "plan": CommPlan JSON | null}]}],
+ *   "pipelines": [[[stage devices]...]...]}  (construct_pipelines' error, if any,
+ * is reported as "pipelines_error" instead). */
+int hs_graph_specialize(const char* graph, int strategy, const char* bindings, char** json);
 
 /* ---------------------------------------------------------------- executor
  * The reference declares execute_plan (sim.hpp:77-79) but never defines it;

@@ -43,6 +43,7 @@
 #include "hshard/deduction.hpp"
 #include "hshard/graph.hpp"
 #include "hshard/resolve.hpp"
+#include "hshard/specialize.hpp"
 #include "hshard/tensor.hpp"
 
 using namespace hshard;
@@ -540,7 +541,7 @@ std::string cmd_execute(const std::vector<std::string>& f) {
 // G|stmt&stmt&...: build the reference CompGraph from the line form of
 // include/hshard/graph.hpp (parse_graph), deduce every strategy with the
 // reference deduce_graph (deduction.cpp:318-353), print the slots.
-std::string cmd_graph(const std::string& program) {
+CompGraph parse_program(const std::string& program) {
   CompGraph g;
   bool first = true;
   for (const std::string& raw : split(program, '&')) {
@@ -585,6 +586,11 @@ std::string cmd_graph(const std::string& program) {
     }
     first = false;
   }
+  return g;
+}
+
+std::string cmd_graph(const std::string& program) {
+  CompGraph g = parse_program(program);
   std::string o = "{\"topo\":" + jints(g.topo_order()) + ",\"strategies\":[";
   for (int s = 0; s < g.strategy_count(); ++s) {
     if (s) o += ",";
@@ -599,6 +605,50 @@ std::string cmd_graph(const std::string& program) {
     }
   }
   return o + "]}";
+}
+
+// S|strategy|bindings|program: the reference's node_phases, instantiate_all
+// and construct_pipelines (specialize.cpp:31-270) on a deduced strategy.
+std::string cmd_specialize(const std::vector<std::string>& f, const std::string& line) {
+  const int strategy = std::stoi(f.at(1));
+  std::map<std::string, int64_t> bind;
+  for (const auto& kv : split(f.at(2), ','))
+    if (!trim(kv).empty()) bind[trim(split(kv, '=').at(0))] = std::stoll(split(kv, '=').at(1));
+  const size_t at = line.find('|', line.find('|', line.find('|') + 1) + 1);
+  CompGraph g = parse_program(line.substr(at + 1));
+  deduce_graph(g, strategy);
+  std::string o = "{\"phases\":{";
+  bool first = true;
+  for (const auto& [id, ph] : node_phases(g, strategy)) {
+    o += std::string(first ? "" : ",") + "\"" + std::to_string(id) + "\":" + jstr(exec_phase_name(ph));
+    first = false;
+  }
+  o += "},\"exec_graphs\":[";
+  const auto egs = instantiate_all(g, strategy, bind);
+  for (size_t i = 0; i < egs.size(); ++i) {
+    o += std::string(i ? "," : "") + "{\"device\":" + std::to_string(egs[i].device) + ",\"nodes\":[";
+    for (size_t k = 0; k < egs[i].nodes.size(); ++k) {
+      const auto& n = egs[i].nodes[k];
+      o += std::string(k ? "," : "") + "{\"node\":" + std::to_string(n.node_id) + ",\"comm\":" +
+           (n.is_comm ? "1" : "0") + ",\"phase\":" + jstr(exec_phase_name(n.phase)) + ",\"plan\":" +
+           (n.plan ? jplan(*n.plan, dtype_name(n.plan->dtype)) : std::string("null")) + "}";
+    }
+    o += "]}";
+  }
+  o += "]";
+  try {
+    const auto pipes = construct_pipelines(g, strategy, bind);
+    o += ",\"pipelines\":[";
+    for (size_t p = 0; p < pipes.size(); ++p) {
+      o += p ? ",[" : "[";
+      for (size_t st = 0; st < pipes[p].stages.size(); ++st) o += std::string(st ? "," : "") + jints(pipes[p].stages[st]);
+      o += "]";
+    }
+    o += "]";
+  } catch (const Error& e) {
+    o += ",\"pipelines_error\":" + jstr(errc_name(e.code()));
+  }
+  return o + "}";
 }
 
 std::string handle(const std::string& line, std::istream& in) {
@@ -671,6 +721,7 @@ std::string handle(const std::string& line, std::istream& in) {
   }
   if (c == "X") return cmd_execute(f);
   if (c == "G") return cmd_graph(line.substr(2));
+  if (c == "S") return cmd_specialize(f, line);
   return "{\"error\":\"UnknownCommand\"}";
 }
 

@@ -60,6 +60,7 @@ def _load() -> ctypes.CDLL:
         # strategy source
         "hs_graph_deduce": (c_int, [c_char_p, P(c_void_p)]),
         "hs_graph_diff": (c_int, [c_char_p, c_int, c_int, c_char_p, P(c_void_p)]),
+        "hs_graph_specialize": (c_int, [c_char_p, c_int, c_char_p, P(c_void_p)]),
         # executor
         "hs_ctx_create": (c_int, [c_int, c_int, c_int, c_size_t, P(c_void_p)]),
         "hs_ctx_destroy": (None, [c_void_p]),

@@ -5,14 +5,15 @@
     python -m paper_2504_20490_b200.cli switch-plan --graph g.json --strategy A --strategy B [--bindings B=8]
     python -m paper_2504_20490_b200.cli report      --plan plan.json [--devices-per-node 8]
     python -m paper_2504_20490_b200.cli simulate    --plan plan.json --input x.bin --out DIR   (B200)
+    python -m paper_2504_20490_b200.cli specialize  --graph g.json --strategy S [--bindings B=8]
+    python -m paper_2504_20490_b200.cli pipelines   --graph g.json --strategy S [--bindings B=8]
 
 Annotations (--src / --dst) are annotation JSON files, inline annotation
 JSON, or the annotation text form; graphs are graph JSON v1; tensors use the
 binary format of formats.py.  Every JSON output carries "version".  Exit 0 on
 success, 1 with a structured error report {"version", "error": {"module",
 "op", "code", "message"}} on a failure, 2 on a usage error (including an
-unknown subcommand).  `specialize` and `pipelines` are outside the
-resharding path and fail with UnsupportedOp.
+unknown subcommand).
 """
 from __future__ import annotations
 
@@ -180,14 +181,34 @@ def cmd_simulate(a):
         ctx.close()
 
 
-def cmd_out_of_scope(a):
-    raise H.HshardError("UnsupportedOp", f"'{a.cmd}' (executable-graph specialization) is outside the resharding "
-                                         "path this library implements (DESIGN.md §8)")
+def _specialized(a):
+    g = F.graph_from_json(_read_json_arg(a.graph))
+    if not a.strategy:
+        raise H.HshardError("ParseError", f"{a.cmd} needs --strategy")
+    s = int(a.strategy[0])
+    return s, g.specialize(s, _bindings(a.bindings))
+
+
+def cmd_specialize(a):
+    """One ExecGraph JSON per device: nodes with their phase and resolved CommPlans."""
+    s, r = _specialized(a)
+    _emit({"version": F.VERSION, "strategy": s, "phases": r["phases"],
+           "exec_graphs": [{**e, "strategy": s} for e in r["exec_graphs"]]}, a.out)
+
+
+def cmd_pipelines(a):
+    """Pipeline structure JSON: stages of device groups per pipeline."""
+    s, r = _specialized(a)
+    if "pipelines_error" in r:
+        raise H.HshardError(r["pipelines_error"], "the strategy's communication is not a set of pipelines")
+    rows = [(p, st, ",".join(map(str, devs))) for p, pipe in enumerate(r["pipelines"]) for st, devs in enumerate(pipe)]
+    _emit({"version": F.VERSION, "strategy": s, "pipelines": r["pipelines"]}, a.out,
+          F.table(rows, ["pipeline", "stage", "devices"]))
 
 
 COMMANDS = {"deduce": cmd_deduce, "plan-comm": cmd_plan_comm, "switch-plan": cmd_switch_plan,
-            "report": cmd_report, "simulate": cmd_simulate, "specialize": cmd_out_of_scope,
-            "pipelines": cmd_out_of_scope}
+            "report": cmd_report, "simulate": cmd_simulate, "specialize": cmd_specialize,
+            "pipelines": cmd_pipelines}
 
 
 def parser():
@@ -213,7 +234,8 @@ def parser():
 def main(argv=None) -> int:
     a = parser().parse_args(argv)  # usage errors exit 2
     need = {"deduce": ["graph"], "plan-comm": ["src", "dst", "shape"], "switch-plan": ["graph"],
-            "report": ["plan"], "simulate": ["plan", "input", "out"]}.get(a.cmd, [])
+            "report": ["plan"], "simulate": ["plan", "input", "out"], "specialize": ["graph", "strategy"],
+            "pipelines": ["graph", "strategy"]}.get(a.cmd, [])
     missing = [f"--{n}" for n in need if getattr(a, n) is None]
     if missing:
         parser().print_usage(sys.stderr)

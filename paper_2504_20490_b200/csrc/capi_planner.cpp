@@ -8,6 +8,7 @@
 #include "capi_common.hpp"
 #include "hshard/deduction.hpp"
 #include "hshard/graph.hpp"
+#include "hshard/specialize.hpp"
 #include "hshard/resolve.hpp"
 #include "hshard/switch.hpp"
 
@@ -233,6 +234,49 @@ int hs_graph_diff(const char* graph, int a, int b, const char* bindings, char** 
            quoted(e.dst.str()) + ",\"shape\":[" + join_ints(e.shape) + "]}";
     }
     *json = capi::dup_string(o + "]");
+  });
+}
+
+int hs_graph_specialize(const char* graph, int strategy, const char* bindings, char** json) {
+  return capi::guarded([&] {
+    CompGraph g = parse_graph(graph);
+    deduce_graph(g, strategy);
+    const auto bind = parse_bindings(bindings);
+    std::string o = "{\"phases\":{";
+    bool first = true;
+    for (const auto& [id, ph] : node_phases(g, strategy)) {
+      o += std::string(first ? "" : ",") + "\"" + std::to_string(id) + "\":" + quoted(exec_phase_name(ph));
+      first = false;
+    }
+    o += "},\"exec_graphs\":[";
+    const auto egs = instantiate_all(g, strategy, bind);
+    for (size_t i = 0; i < egs.size(); ++i) {
+      o += std::string(i ? "," : "") + "{\"device\":" + std::to_string(egs[i].device) + ",\"nodes\":[";
+      for (size_t k = 0; k < egs[i].nodes.size(); ++k) {
+        const ExecNode& n = egs[i].nodes[k];
+        o += std::string(k ? "," : "") + "{\"node\":" + std::to_string(n.node_id) + ",\"comm\":" +
+             (n.is_comm ? "1" : "0") + ",\"phase\":" + quoted(exec_phase_name(n.phase)) +
+             ",\"plan\":" + (n.plan ? dump_plan(*n.plan) : std::string("null")) + "}";
+      }
+      o += "]}";
+    }
+    o += "]";
+    try {
+      const auto pipes = construct_pipelines(g, strategy, bind);
+      o += ",\"pipelines\":[";
+      for (size_t p = 0; p < pipes.size(); ++p) {
+        o += p ? ",[" : "[";
+        for (size_t st = 0; st < pipes[p].stages.size(); ++st) {
+          std::vector<int64_t> devs(pipes[p].stages[st].begin(), pipes[p].stages[st].end());
+          o += std::string(st ? "," : "") + "[" + join_ints(devs) + "]";
+        }
+        o += "]";
+      }
+      o += "]";
+    } catch (const Error& e) {
+      o += ",\"pipelines_error\":" + quoted(errc_name(e.code()));
+    }
+    *json = capi::dup_string(o + "}");
   });
 }
 

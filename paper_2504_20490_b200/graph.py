@@ -99,6 +99,14 @@ class Graph:
         check(LIB.hs_graph_diff(self.text().encode(), a, b, bind.encode(), out))
         return json.loads(take_string(out))
 
+    def specialize(self, strategy: int, bindings: Optional[Dict[str, int]] = None) -> dict:
+        """Executable graphs per device, node phases and pipelines of one strategy
+        (reference specialize.hpp): {"phases", "exec_graphs", "pipelines" | "pipelines_error"}."""
+        out = c_void_p()
+        bind = ",".join(f"{k}={v}" for k, v in (bindings or {}).items())
+        check(LIB.hs_graph_specialize(self.text().encode(), strategy, bind.encode(), out))
+        return json.loads(take_string(out))
+
     def switch_plan(self, a: int, b: int, dtype: str = "bf16", bindings: Optional[Dict[str, int]] = None,
                     bandwidth: str = "u") -> H.Plan:
         """plan_switch over diff(a, b): the fused Bsr plan that moves the weights."""

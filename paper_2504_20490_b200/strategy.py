@@ -4,8 +4,9 @@ SPEC.md:413-418).
 
 A Llama-shaped block graph is built once with one annotation slot per named
 strategy; leaves (the one-hot token batch and every weight) and CommOps (the
-all-reduces after row-parallel matmuls, and stage hand-offs under pipeline
-parallelism) are annotated, everything else is deduced.  diff_strategies
+all-reduces after row-parallel matmuls, and the hand-off to the next layer's
+devices -- a pipeline send at stage edges) are annotated, everything else is
+deduced, and specialize / construct_pipelines recover each strategy's stages.  diff_strategies
 between two slots yields exactly the parameter moves plan_switch executes --
 the same (src, dst) pairs workloads.config4 / config5 spell out by hand.
 
@@ -86,8 +87,9 @@ def llama_graph(layers: int, hidden: int, ffn: int, vocab: int, strategies: Dict
         down = param(f"l{l}.down", [ffn, hidden], 0, l, "layer")
         a = g.elementwise("gelu", g.dot(h, gate))
         g.dot(h, up)
-        # all-reduce, landing on the next layer's stage (a pipeline hand-off at stage edges)
-        h = comm(g.dot(a, down), l + 1, "layer") if l + 1 < layers else comm(g.dot(a, down), None, "head")
+        h = comm(g.dot(a, down), l, "layer")  # row-parallel -> all-reduce on this layer's devices
+        # hand-off to the next layer's devices: a pipeline send at stage edges, identity elsewhere
+        h = comm(h, l + 1, "layer") if l + 1 < layers else comm(h, None, "head")
     param("final_norm", [hidden], -1, None, "head")
     head = param("lm_head", [hidden, vocab], 1, None, "head")
     g.dot(h, head)

@@ -164,6 +164,15 @@ def handwritten():
         "annotate 0 0 hsize=1 hdim=-1 [(0,1){-2:2}]", "annotate 1 0 hsize=1 hdim=-1 [(0,1){-2:2}]",
         "annotate 0 1 hsize=1 hdim=-1 [(0,1){5:2}]", "annotate 1 1 hsize=1 hdim=-1 [(0,1){-1:2}]",
         "annotate 0 2 hsize=1 hdim=-1 [(0,1){-1:2}]"]))
+    # pipelines: a forward hand-off 0 -> 1 and a second one back 1 -> 0 make
+    # device 1 both one stage after and one stage before device 0
+    # (ConflictingStageOrder); a plain 0 -> 1 -> 2 chain is three stages
+    g.append("\n".join([
+        "strategies 2", "placeholder x f32 8 8", "comm 0 0", "elementwise relu 1", "comm 2 0",
+        "annotate 0 0 hsize=1 hdim=-1 [(0){}]", "annotate 1 0 hsize=1 hdim=-1 [(1){}]",
+        "annotate 3 0 hsize=1 hdim=-1 [(0){}]",
+        "annotate 0 1 hsize=1 hdim=-1 [(0){}]", "annotate 1 1 hsize=1 hdim=-1 [(1){}]",
+        "annotate 3 1 hsize=1 hdim=-1 [(2){}]"]))
     return g
 
 

@@ -41,7 +41,8 @@ def test_cpp_api_symbols_exported():
                 "hshard::top_resolve(", "hshard::execute_plan(", "hshard::apply_switch(",
                 "hshard::plan_switch(", "hshard::reassemble(", "hshard::scatter(",
                 "hshard::volume_report(", "hshard::Tensor::slice(", "hshard::deduce_graph(",
-                "hshard::CompGraph::dot(", "hshard::unify_inputs(", "hshard::diff_strategies(hshard::CompGraph"]:
+                "hshard::CompGraph::dot(", "hshard::unify_inputs(", "hshard::diff_strategies(hshard::CompGraph",
+                "hshard::instantiate(", "hshard::construct_pipelines(", "hshard::assign_schedule("]:
         assert sym in out, sym
 
 

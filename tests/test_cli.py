@@ -125,7 +125,7 @@ def test_exit_codes(tmp_path):
             "--shape", "8,8", check_rc=1)
     err = json.loads(r.stdout)["error"]
     assert err["code"] == "PartialUnderBsr" and err["module"] == "plan-comm"
-    assert json.loads(cli("specialize", check_rc=1).stdout)["error"]["code"] == "UnsupportedOp"
+    assert cli("specialize").returncode == 2  # needs --graph and --strategy
     bad = tmp_path / "g.json"
     bad.write_text(json.dumps({"version": "v0", "nodes": []}))
     assert json.loads(cli("deduce", "--graph", str(bad), check_rc=1).stdout)["error"]["code"] == "ParseError"
@@ -150,3 +150,17 @@ def test_simulate_on_b200(tmp_path):
         got, _ = F.read_tensor(str(out / s["file"]))
         box = tuple(slice(lo, hi) for lo, hi in s["bounds"])
         assert np.array_equal(got, x[box]), d
+
+
+def test_specialize_and_pipelines(tmp_path):
+    st = {"A": tp_pp(2, 2, 2), "B": tp_pp(2, 4, 4)}
+    g, n = llama_graph(4, 64, 128, 256, {"A": tp_pp(2, 2, 4), "P": tp_pp(2, 4, 4)}, dtype="f32")
+    path = tmp_path / "g.json"
+    path.write_text(json.dumps(F.graph_to_json(g)))
+    sp = json.loads(cli("specialize", "--graph", str(path), "--strategy", "1", "--bindings", "B=8",
+                        check_rc=0).stdout)
+    assert [e["device"] for e in sp["exec_graphs"]] == list(range(8))
+    assert all(node["plan"] is not None for e in sp["exec_graphs"] for node in e["nodes"] if node["comm"])
+    r = cli("pipelines", "--graph", str(path), "--strategy", "1", "--bindings", "B=8", check_rc=0)
+    assert json.loads(r.stdout)["pipelines"] == [[[0, 1], [2, 3], [4, 5], [6, 7]]]
+    assert "stage" in r.stderr

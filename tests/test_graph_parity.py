@@ -144,3 +144,25 @@ def test_switch_plan_from_graph_conserves_bytes():
                 dst += cells(H.placement(e["dst"], e["shape"], d)["bounds"]) * 2
     assert moved + local == dst
     assert abs(moved / 1e9 - 10.108) < 0.001  # 10.108 GB of transfers for cfg4
+
+
+def test_golden_specialization():
+    """instantiate_all / node_phases / construct_pipelines vs the reference's
+    (ref_tool S; tests/golden/specialize.jsonl): executable graphs per device,
+    the CommPlan each CommOp resolves to, phases and pipeline stages."""
+    from ctypes import c_void_p
+    cases = [json.loads(l) for l in open(os.path.join(HERE, "golden", "specialize.jsonl"))]
+    assert len(cases) >= 150
+    bad = []
+    for c in cases:
+        out = c_void_p()
+        rc = LIB.hs_graph_specialize(c["graph"].encode(), c["strategy"], c["bindings"].encode(), out)
+        mine = {"error": ERRC_NAMES[rc - 1]} if rc else json.loads(take_string(out))
+        if mine != c["out"]:
+            bad.append((c["strategy"], c["graph"][:200]))
+    assert not bad, f"{len(bad)} mismatches, first: {bad[0]}"
+    # the Llama graph recovers each strategy's pipeline structure
+    pipes = [c["out"]["pipelines"] for c in cases[:5]]
+    assert pipes == [[[list(range(8))]], [[[0, 1, 2, 3]], [[4, 5, 6, 7]]], [[[0, 1, 2, 3]], [[4, 5]], [[6, 7]]],
+                     [[[0, 1, 2, 3], [4, 5, 6, 7]]], [[[0, 1], [2, 3], [4, 5], [6, 7]]]]
+    assert any("pipelines_error" in c["out"] for c in cases)  # ConflictingStageOrder is exercised
