@@ -162,6 +162,14 @@ int hs_prog_run(hs_prog* prog, void* stream);
  * source shards from host pointers (indexed by virtual id; NULL = skip),
  * run, D2H of destination shards.  Synchronous. */
 int hs_prog_run_host(hs_prog* prog, const void* const* src_host, void* const* dst_host);
+/* The same, enqueued without synchronising: H2D on `h2d` (cudaStream_t),
+ * the run on `compute` after it, D2H on `d2h` after the run (events order the
+ * three streams).  A caller double-buffers steps with two programs over two
+ * shard layouts sharing one compute stream (runs, and their barriers, stay in
+ * order) so step k+1's H2D overlaps step k's run and D2H on a full-duplex
+ * link.  Completion: synchronise `d2h`. */
+int hs_prog_run_host_async(hs_prog* prog, const void* const* src_host, void* const* dst_host, void* h2d,
+                           void* compute, void* d2h);
 /* Per-phase kernel timing with CUDA events on the launching stream (bench /
  * roofline evidence).  hs_prog_profile(1) resets and enables; every run then
  * records 2 events per phase; hs_prog_phase_ms sums elapsed ms per phase over

@@ -76,6 +76,7 @@ def _load() -> ctypes.CDLL:
         "hs_prog_destroy": (None, [c_void_p]),
         "hs_prog_run": (c_int, [c_void_p, c_void_p]),
         "hs_prog_run_host": (c_int, [c_void_p, P(c_void_p), P(c_void_p)]),
+        "hs_prog_run_host_async": (c_int, [c_void_p, P(c_void_p), P(c_void_p), c_void_p, c_void_p, c_void_p]),
         "hs_prog_stats": (c_int, [c_void_p, P(c_void_p)]),
         "hs_prog_profile": (c_int, [c_void_p, c_int]),
         "hs_prog_phase_ms": (c_int, [c_void_p, P(ctypes.c_double), c_int, P(c_int)]),

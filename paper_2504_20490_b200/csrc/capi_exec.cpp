@@ -114,6 +114,14 @@ int hs_prog_run(hs_prog* prog, void* stream) {
   return guarded([&] { prog->p->run(static_cast<cudaStream_t>(stream)); });
 }
 
+int hs_prog_run_host_async(hs_prog* prog, const void* const* src_host, void* const* dst_host, void* h2d,
+                           void* compute, void* d2h) {
+  return guarded([&] {
+    prog->p->run_host_async(src_host, dst_host, static_cast<cudaStream_t>(h2d), static_cast<cudaStream_t>(compute),
+                            static_cast<cudaStream_t>(d2h));
+  });
+}
+
 int hs_prog_run_host(hs_prog* prog, const void* const* src_host, void* const* dst_host) {
   return guarded([&] { prog->p->run_host(src_host, dst_host); });
 }

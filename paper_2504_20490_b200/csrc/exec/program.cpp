@@ -128,6 +128,8 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
 
 Program::~Program() {
   if (dev_block_) cudaFree(dev_block_);
+  for (cudaEvent_t e : host_ev_)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : events_) cudaEventDestroy(e);
 }
 
@@ -1397,6 +1399,32 @@ void Program::run(cudaStream_t s) {
     if (profiling_) event();
   }
   if (remote_final_writes_ && !nccl_mode_) ctx_.barrier(s);
+}
+
+void Program::run_host_async(const void* const* src_host, void* const* dst_host, cudaStream_t h2d,
+                             cudaStream_t compute, cudaStream_t d2h) {
+  // [0] inputs landed, [1] run done, [2] outputs read.  A repeated call waits
+  // for its previous run to finish reading the sources before overwriting them,
+  // and for its previous D2H before the run overwrites the destinations (an
+  // event never recorded is already complete).
+  for (cudaEvent_t& e : host_ev_)
+    if (!e) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaStreamWaitEvent(h2d, host_ev_[1], 0), "stream wait");
+  for (const auto& [d, t, off, bytes] : host_src_) {
+    const void* h = src_host[static_cast<size_t>(t) * n_virt_ + d];
+    if (h) cuda_check(cudaMemcpyAsync(ctx_.arena() + off, h, bytes, cudaMemcpyHostToDevice, h2d), "H2D");
+  }
+  cuda_check(cudaEventRecord(host_ev_[0], h2d), "event record");
+  cuda_check(cudaStreamWaitEvent(compute, host_ev_[0], 0), "stream wait");
+  cuda_check(cudaStreamWaitEvent(compute, host_ev_[2], 0), "stream wait");
+  run(compute);
+  cuda_check(cudaEventRecord(host_ev_[1], compute), "event record");
+  cuda_check(cudaStreamWaitEvent(d2h, host_ev_[1], 0), "stream wait");
+  for (const auto& [d, t, off, bytes] : host_dst_) {
+    void* h = dst_host[static_cast<size_t>(t) * n_virt_ + d];
+    if (h) cuda_check(cudaMemcpyAsync(h, ctx_.arena() + off, bytes, cudaMemcpyDeviceToHost, d2h), "D2H");
+  }
+  cuda_check(cudaEventRecord(host_ev_[2], d2h), "event record");
 }
 
 void Program::run_host(const void* const* src_host, void* const* dst_host) {

@@ -149,6 +149,8 @@ class Program {
 
   void run(cudaStream_t s);
   void run_host(const void* const* src_host, void* const* dst_host);
+  void run_host_async(const void* const* src_host, void* const* dst_host, cudaStream_t h2d, cudaStream_t compute,
+                      cudaStream_t d2h);
   // Profiling: when enabled, run() brackets each phase's launches with CUDA
   // events on the launching stream; phase_ms() sums the elapsed times of all
   // runs since enabling (synchronises) and returns the run count.
@@ -222,6 +224,7 @@ class Program {
   int staging_state_ = 1 << 30;
   std::vector<std::vector<Exchange>> exchanges_;
   std::vector<cudaEvent_t> events_;  // 2 per phase per profiled run
+  cudaEvent_t host_ev_[3] = {nullptr, nullptr, nullptr};  // run_host_async: inputs landed / run done / read
   size_t events_used_ = 0;
   ProgramStats stats_;
   std::vector<BoxTask> analysed_;  // analysis contexts: this rank's final tasks

@@ -244,7 +244,7 @@ class Program:
     """hs_prog: a plan compiled for this rank."""
 
     def __init__(self, ctx: Context, plan: H.Plan, layout: ShardLayout, flags: int = 0):
-        self.ctx, self.plan, self.layout = ctx, plan, layout
+        self.ctx, self.plan, self.layout, self.flags = ctx, plan, layout, flags
         m = (c_int * layout.n_virtual)(*layout.v_to_rank)
         h = c_void_p()
         check(LIB.hs_prog_compile(ctx.handle, plan.handle, m, layout.n_virtual, layout.src_off,
@@ -254,8 +254,7 @@ class Program:
     def run(self, stream=None) -> None:
         check(LIB.hs_prog_run(self._h, stream))
 
-    def run_host(self, src: Dict[Tuple[int, int], np.ndarray], dst: Dict[Tuple[int, int], np.ndarray]):
-        """Host-buffer execution: src/dst keyed by (slot, dev); only this rank's shards are used."""
+    def _host_ptrs(self, src, dst):
         n = len(self.layout.entries) * self.layout.n_virtual
         sp = (c_void_p * max(1, n))()
         dp = (c_void_p * max(1, n))()
@@ -263,7 +262,18 @@ class Program:
             sp[slot * self.layout.n_virtual + dev] = a.ctypes.data
         for (slot, dev), a in dst.items():
             dp[slot * self.layout.n_virtual + dev] = a.ctypes.data
+        return sp, dp
+
+    def run_host(self, src: Dict[Tuple[int, int], np.ndarray], dst: Dict[Tuple[int, int], np.ndarray]):
+        """Host-buffer execution: src/dst keyed by (slot, dev); only this rank's shards are used."""
+        sp, dp = self._host_ptrs(src, dst)
         check(LIB.hs_prog_run_host(self._h, sp, dp))
+
+    def run_host_async(self, src, dst, h2d, compute, d2h) -> None:
+        """run_host enqueued on three CUDA streams (raw cudaStream_t handles); see hs_prog_run_host_async.
+        Host buffers should be pinned; synchronise `d2h` before reading `dst`."""
+        sp, dp = self._host_ptrs(src, dst)
+        check(LIB.hs_prog_run_host_async(self._h, sp, dp, h2d, compute, d2h))
 
     def profile(self, enable: bool = True) -> None:
         check(LIB.hs_prog_profile(self._h, int(enable)))

@@ -191,3 +191,34 @@ def test_host_buffer_path(gpu_ctx):
             assert np.array_equal(a, want[d])
     finally:
         gpu_ctx.reset(mark)
+
+
+def test_host_buffer_path_pipelined(gpu_ctx):
+    """hs_prog_run_host_async: two programs over two layouts alternate on three
+    streams; every step's outputs are that step's inputs resharded."""
+    import torch
+    from paper_2504_20490_b200.executor import Program, ShardLayout
+    w = W.config2("e")
+    tid, src, dst, shape = w.transitions[0]
+    shape = (512, 1024)
+    plan = H.classify(src, dst, shape, "bf16")
+    mark = gpu_ctx.alloc(0)
+    try:
+        lays = [ShardLayout(gpu_ctx, plan, 8) for _ in range(2)]
+        progs = [Program(gpu_ctx, plan, l) for l in lays]
+        streams = [torch.cuda.Stream() for _ in range(3)]
+        h2d, comp, d2h = (s.cuda_stream for s in streams)
+        steps = []
+        for k in range(4):
+            srcs = ox.scatter(src, shape, "bf16", 20 + k, 0, "real")
+            host_src = {(0, d): a for d, a in srcs.items()}
+            host_dst = {(0, d): np.zeros(r["ext"], dtype=np.uint16) for (s, d), r in lays[k % 2].dst.items()}
+            progs[k % 2].run_host_async(host_src, host_dst, h2d, comp, d2h)
+            steps.append((srcs, host_src, host_dst))
+        streams[2].synchronize()
+        for srcs, _, host_dst in steps:
+            want = ox.execute_plan(plan.json(), srcs, "bf16")
+            for (s, d), a in host_dst.items():
+                assert np.array_equal(a, want[d])
+    finally:
+        gpu_ctx.reset(mark)
