@@ -145,9 +145,13 @@ enum {
                                      (no peer-memory access, no device barriers) */,
   HS_PROG_NO_STREAM = 4096,       /* world > 1: two-phase programs keep a barrier between the
                                      phases instead of one launch with per-chunk ready flags */
-  HS_PROG_PULL_MID = 8192         /* world > 1: phase 2 pulls remote mid boxes from the
+  HS_PROG_PULL_MID = 8192,        /* world > 1: phase 2 pulls remote mid boxes from the
                                      producer's HBM (local groups still fused) instead of
                                      relay stores into the consumer's HBM */
+  HS_PROG_CE_RELAY = 16384        /* world > 1: relays move on the copy engines -- producers
+                                     write their HBM in K row chunks, each chunk is copied to
+                                     its consumers by DMA while the SMs continue, consumers of a
+                                     chunk wait for it (implies NO_SHARE | PULL_COPIES) */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

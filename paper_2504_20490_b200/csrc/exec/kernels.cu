@@ -925,6 +925,30 @@ __global__ void barrier_kernel(unsigned int* const* peer_flags, int world, int r
   __threadfence_system();
 }
 
+__global__ void signal_kernel(unsigned int* const* targets, int n, unsigned int epoch) {
+  // stream order: the copies before this kernel have completed
+  __threadfence_system();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(targets[i]), "r"(epoch) : "memory");
+}
+
+__global__ void wait_flags_kernel(const unsigned int* const* flags, int n, unsigned int epoch,
+                                  unsigned long long timeout_ns, int* error) {
+  const unsigned long long t0 = global_ns();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags[i]) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      if (*reinterpret_cast<volatile int*>(error) || global_ns() - t0 > timeout_ns) {
+        *error = 1;
+        break;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
 int grid_for(int64_t work, int per_block) {
   int64_t g = (work + per_block - 1) / per_block;
   if (g > 148 * 8) g = 148 * 8;
@@ -1027,6 +1051,19 @@ cudaError_t launch_verify(const FillDesc& f, int dtype, unsigned long long* bad,
   for (int d = 0; d < f.ndim; ++d) cells *= f.ext[d];
   if (cells == 0) return cudaSuccess;
   return by_dtype<VerifyK>(dtype, dim3(grid_for(cells, 256 * 8)), dim3(256), s, f, cells, bad);
+}
+
+cudaError_t launch_signal(unsigned int* const* targets, int n, unsigned int epoch, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  signal_kernel<<<1, 32, 0, s>>>(targets, n, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const unsigned int* const* flags, int n, unsigned int epoch,
+                              unsigned long long timeout_ns, int* error, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  wait_flags_kernel<<<1, 32, 0, s>>>(flags, n, epoch, timeout_ns, error);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_barrier(unsigned int* const* peer_flags, int world, int rank,

@@ -144,4 +144,12 @@ cudaError_t launch_barrier(unsigned int* const* peer_flags, int world, int rank,
                            unsigned int epoch, unsigned long long timeout_ns, int* error,
                            cudaStream_t s);
 
+// Copy-engine relays: after the copies of a chunk, the sender's copy stream
+// stores `epoch` (st.release.sys) into each receiver's flag word; the
+// receiver's compute stream spins (ld.acquire.sys, bounded) until all its
+// senders' words reach `epoch`.  Both are one-warp kernels.
+cudaError_t launch_signal(unsigned int* const* targets, int n, unsigned int epoch, cudaStream_t s);
+cudaError_t launch_wait_flags(const unsigned int* const* flags, int n, unsigned int epoch,
+                              unsigned long long timeout_ns, int* error, cudaStream_t s);
+
 }  // namespace hshard::exec

@@ -130,6 +130,9 @@ Program::~Program() {
   if (dev_block_) cudaFree(dev_block_);
   for (cudaEvent_t e : host_ev_)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ce_events_) cudaEventDestroy(e);
+  if (ce_stream_) cudaStreamDestroy(ce_stream_);
+  if (ce_dev_) cudaFree(ce_dev_);
   for (cudaEvent_t e : events_) cudaEventDestroy(e);
 }
 
@@ -300,6 +303,13 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     flags_ |= HS_PROG_NO_RELAY | HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES;
     flags_ &= ~(HS_PROG_PUSH_ALL | HS_PROG_FUSE_PHASES);
   }
+  ce_mode_ = ctx_.world() > 1 && (flags_ & HS_PROG_CE_RELAY) && !nccl_mode_;
+  if (ce_mode_) {
+    // producers run where their mid box lives; nothing else stores remotely
+    flags_ |= HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES;
+    flags_ &= ~(HS_PROG_PUSH_ALL | HS_PROG_FUSE_PHASES | HS_PROG_PULL_MID | HS_PROG_NO_RELAY);
+    if (const char* e = std::getenv("HS_CE_CHUNKS")) ce_chunks_ = std::max(1, std::atoi(e));
+  }
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
@@ -346,11 +356,13 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
                                                                  : RelayMode::FuseLocal;
     tasks = finish(fuse_phases(std::move(tasks), mode));
     stats_.model_ms[0] = estimate_seconds(tasks, n_phases_) * 1e3;
+    if (ce_mode_) tasks = ce_relay(std::move(tasks));
   } else {
     tasks = finish(std::move(tasks));
   }
 
   if (nccl_mode_) stage_for_nccl(tasks);
+  if (ce_mode_ && ce_copies_.empty()) ce_mode_ = false;  // no relay to move
 
   // world > 1: both plan phases in one launch with per-chunk ready flags
   // (kept only if every producer / consumer piece runs on the TMA path).
@@ -411,11 +423,23 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     }
   }
   stats_.streamed = streamed_;
+  if (ce_mode_) {
+    // copy geometry (mid box on the sender == relay box on the receiver, same
+    // region layout) and the symmetric chunk flag words
+    ce_geometry();
+    const size_t bytes = static_cast<size_t>(ctx_.world()) * ce_chunks_ * 4;
+    ce_flag_off_ = ctx_.alloc(bytes + 256);
+    if (!ctx_.is_analysis()) {
+      cuda_check(cudaMemsetAsync(ctx_.arena() + ce_flag_off_, 0, bytes + 256, ctx_.stream()), "memset(ce flags)");
+      cuda_check(cudaStreamSynchronize(ctx_.stream()), "memset(ce flags) sync");
+    }
+  }
+  stats_.ce_relay = ce_mode_;
 
   // Stores into peers' destination shards in the last launch need a closing
   // barrier (relay / intermediate stores are consumed inside the run).
   for (const BoxTask& t : tasks)
-    if (t.phase == n_phases_ - 1)
+    if (t.phase == n_phases_ - 1 || ce_mode_)
       for (const Operand& o : t.dsts)
         remote_final_writes_ = remote_final_writes_ ||
                                (o.state == static_cast<int>(final_state_) && rank_of(o, t.tensor) != t.rank);
@@ -457,6 +481,11 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     }
     if (mine_task) mine.push_back(std::move(t));
   }
+  for (const CeCopy& c : ce_copies_) {
+    const int64_t b = static_cast<int64_t>(c.width * c.height * c.planes);
+    if (c.sender == me) stats_.nvlink_out += b;
+    if (c.receiver == me) stats_.nvlink_in += b;
+  }
   if (ctx_.is_analysis()) analysed_ = mine;
   for (const BoxTask& t : mine) {
     for (const Operand& o : t.dsts)
@@ -467,6 +496,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
         fail(Errc::MissingShard, "source shard of device " + std::to_string(o.dev) + " has no buffer");
   }
   build_tables(mine);
+  if (ce_mode_ && !ctx_.is_analysis()) ce_build();
 }
 
 // ---------------------------------------------------------------- replicas
@@ -919,6 +949,180 @@ std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks) {
     out.push_back(std::move(t));
   }
   return out;
+}
+
+// ---------------------------------------------------------------- copy-engine relays
+// HS_PROG_CE_RELAY: an SM moves only ~5-6 GB/s over NVLink (loads or stores),
+// so NVLink-bound and HBM-bound work compete for SMs; the copy engines move
+// 650+ GB/s with no SM and no HBM-rate loss (measured, tools/ce_probe.py).
+// Relay producers therefore write their result into their own mid box, in K
+// row chunks (one launch each); after chunk k the rank's copy stream copies
+// it into every consumer's relay buffer (2-D DMA from the same offsets) and
+// signals the consumer; the consumers of chunk k wait for that signal.  The
+// phases become: [0, K) producer chunks, K the other phase-1 work (runs while
+// the DMA moves), K+1+k consumers of chunk k, 2K+1 the other phase-2 work.
+std::vector<BoxTask> Program::ce_relay(std::vector<BoxTask> tasks) {
+  const int W = ctx_.world(), K = ce_chunks_;
+  auto is_relay = [&](int st) { return st > static_cast<int>(final_state_) && st < staging_state_; };
+  bool any = false;
+  for (const BoxTask& t : tasks)
+    for (const Operand& o : t.dsts) any = any || is_relay(o.state);
+  if (!any) return tasks;
+  const int64_t rows = shapes_.at(0).at(0);
+  std::vector<int64_t> cut(K + 1);
+  for (int k = 0; k <= K; ++k) cut[k] = rows * k / K;
+  std::vector<BoxTask> out;
+  for (BoxTask& t : tasks) {
+    bool prod = false, cons = false;
+    for (const Operand& o : t.dsts) prod = prod || is_relay(o.state);
+    for (const Operand& o : t.terms) cons = cons || is_relay(o.state);
+    if (!prod && !cons) {
+      t.phase = t.phase == 0 ? K : 2 * K + 1;
+      out.push_back(std::move(t));
+      continue;
+    }
+    const int64_t lo = t.box.bounds[0][0], hi = t.box.bounds[0][1];
+    for (int64_t a = lo; a < hi;) {
+      const int k = static_cast<int>(std::upper_bound(cut.begin(), cut.end(), a) - cut.begin()) - 1;
+      const int64_t b = std::min(hi, cut[k + 1]);
+      BoxTask piece = t;
+      piece.box.bounds[0] = {a, b};
+      if (prod) {
+        std::vector<Operand> dsts;
+        for (const Operand& o : t.dsts) {
+          if (!is_relay(o.state)) {
+            dsts.push_back(o);
+            continue;
+          }
+          const DeviceId c = o.dev / W;
+          const int q = static_cast<int>(o.dev % W);
+          const Operand mid{mid_state_, c};
+          if (loc(mid_state_, 0, c).rank != piece.rank)
+            fail(Errc::UnsupportedOp, "copy-engine relay: producer not on its mid box's rank");
+          if (std::find(dsts.begin(), dsts.end(), mid) == dsts.end()) dsts.push_back(mid);
+          CeCopy cp{};
+          cp.chunk = k;
+          cp.sender = piece.rank;
+          cp.receiver = q;
+          // geometry: filled once offsets exist (ce_geometry below); keep the
+          // operands in the offsets for now
+          cp.src_off = static_cast<size_t>(c);
+          cp.dst_off = static_cast<size_t>(o.dev);
+          cp.planes = static_cast<size_t>(o.state);
+          ce_boxes_.push_back(piece.box);
+          ce_mid_dev_.push_back(c);
+          ce_relay_dev_.push_back(o.dev);
+          ce_copies_.push_back(cp);
+        }
+        piece.dsts = std::move(dsts);
+        piece.phase = k;
+      } else {
+        piece.phase = K + 1 + k;
+      }
+      out.push_back(std::move(piece));
+      a = b;
+    }
+  }
+  n_phases_ = 2 * K + 2;
+  return out;
+}
+
+void Program::ce_geometry() {
+  for (size_t i = 0; i < ce_copies_.size(); ++i) {
+    CeCopy& c = ce_copies_[i];
+    const DeviceId mid_dev = static_cast<DeviceId>(c.src_off), relay_dev = static_cast<DeviceId>(c.dst_off);
+    const int relay_state = static_cast<int>(c.planes);
+    const ShardLoc& S = loc(mid_state_, 0, mid_dev);
+    const ShardLoc& D = loc(relay_state, 0, relay_dev);
+    const SliceRegion& box = ce_boxes_[i];
+    const std::vector<int64_t> st = row_major_strides(S.region.extents());
+    int64_t off = 0;
+    for (size_t d = 0; d < box.bounds.size(); ++d) off += (box.bounds[d][0] - S.region.bounds[d][0]) * st[d];
+    // merge dims contiguous in the region, drop unit outer dims
+    std::vector<int64_t> ext, str;
+    const Shape e = box.extents();
+    for (size_t d = 0; d < e.size(); ++d) {
+      if (e[d] == 1 && d + 1 < e.size()) continue;
+      if (!ext.empty() && str.back() == e[d] * st[d]) {
+        ext.back() *= e[d];
+        str.back() = st[d];
+        continue;
+      }
+      ext.push_back(e[d]);
+      str.push_back(st[d]);
+    }
+    if (ext.size() > 3) fail(Errc::UnsupportedOp, "copy-engine relay of a box with more than 3 strided dims");
+    while (ext.size() < 3) {
+      ext.insert(ext.begin(), 1);
+      str.insert(str.begin(), 0);
+    }
+    c.planes = static_cast<size_t>(ext[0]);
+    c.plane_stride = static_cast<size_t>(str[0] * es_);
+    c.height = static_cast<size_t>(ext[1]);
+    c.pitch = static_cast<size_t>((ext[1] > 1 ? str[1] : ext[2]) * es_);
+    c.width = static_cast<size_t>(ext[2] * es_);
+    c.src_off = S.offset + static_cast<size_t>(off * es_);
+    c.dst_off = D.offset + static_cast<size_t>(off * es_);
+  }
+}
+
+void Program::ce_build() {
+  const int me = ctx_.rank(), K = ce_chunks_;
+  std::vector<std::set<int>> to(K), from(K);
+  for (const CeCopy& c : ce_copies_) {
+    if (c.sender == me) to[c.chunk].insert(c.receiver);
+    if (c.receiver == me) from[c.chunk].insert(c.sender);
+  }
+  auto word = [&](int rank, int sender, int k) {
+    return reinterpret_cast<unsigned int*>(ctx_.arena_of(rank) + ce_flag_off_) + sender * K + k;
+  };
+  std::vector<unsigned int*> host;
+  std::vector<size_t> t0(K), w0(K);
+  ce_ntargets_.assign(K, 0);
+  ce_nwaits_.assign(K, 0);
+  for (int k = 0; k < K; ++k) {
+    t0[k] = host.size();
+    for (int q : to[k]) host.push_back(word(q, me, k));
+    ce_ntargets_[k] = static_cast<int>(to[k].size());
+    w0[k] = host.size();
+    for (int p : from[k]) host.push_back(word(me, p, k));
+    ce_nwaits_[k] = static_cast<int>(from[k].size());
+  }
+  cuda_check(cudaMalloc(&ce_dev_, std::max<size_t>(1, host.size()) * sizeof(unsigned int*)), "cudaMalloc(ce)");
+  cuda_check(cudaMemcpy(ce_dev_, host.data(), host.size() * sizeof(unsigned int*), cudaMemcpyHostToDevice),
+             "cudaMemcpy(ce)");
+  auto* base = static_cast<unsigned int**>(ce_dev_);
+  ce_targets_.resize(K);
+  ce_waits_.resize(K);
+  for (int k = 0; k < K; ++k) {
+    ce_targets_[k] = base + t0[k];
+    ce_waits_[k] = const_cast<const unsigned int**>(base + w0[k]);
+  }
+  cuda_check(cudaStreamCreateWithFlags(&ce_stream_, cudaStreamNonBlocking), "cudaStreamCreate(ce)");
+  ce_events_.resize(K);
+  for (cudaEvent_t& e : ce_events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event(ce)");
+  int signals = 0, waits = 0;
+  for (int k = 0; k < K; ++k) {
+    signals += ce_ntargets_[k] > 0;
+    waits += ce_nwaits_[k] > 0;
+  }
+  stats_.kernels_per_run += signals + waits - n_phases_ + 1;  // one barrier per run, not one per phase
+}
+
+void Program::ce_run_phase_post(int k, cudaStream_t s) {
+  const int me = ctx_.rank();
+  if (!ce_ntargets_[k]) return;
+  cuda_check(cudaEventRecord(ce_events_[k], s), "event record(ce)");
+  cuda_check(cudaStreamWaitEvent(ce_stream_, ce_events_[k], 0), "stream wait(ce)");
+  for (const CeCopy& c : ce_copies_) {
+    if (c.sender != me || c.chunk != k) continue;
+    for (size_t p = 0; p < c.planes; ++p)
+      cuda_check(cudaMemcpy2DAsync(ctx_.arena_of(c.receiver) + c.dst_off + p * c.plane_stride, c.pitch,
+                                   ctx_.arena() + c.src_off + p * c.plane_stride, c.pitch, c.width, c.height,
+                                   cudaMemcpyDeviceToDevice, ce_stream_),
+                 "copy-engine relay");
+  }
+  cuda_check(launch_signal(ce_targets_[k], ce_ntargets_[k], runs_, ce_stream_), "signal launch");
 }
 
 // ---------------------------------------------------------------- streaming
@@ -1374,6 +1578,27 @@ void Program::run(cudaStream_t s) {
   // destinations are complete when its stream is (callers still sync all
   // ranks before modifying sources).
   ++runs_;
+  if (ce_mode_) {
+    const int K = ce_chunks_;
+    ctx_.barrier(s);
+    for (int p = 0; p < n_phases_; ++p) {
+      const int kc = p - K - 1;
+      if (kc >= 0 && kc < K && ce_nwaits_[kc])
+        cuda_check(launch_wait_flags(ce_waits_[kc], ce_nwaits_[kc], runs_, 20ull * 1000 * 1000 * 1000,
+                                     ctx_.error_flag(), s),
+                   "wait launch");
+      if (profiling_) event();
+      for (const Launch& l : dphases_[p].launches) {
+        PhaseTables t = l.tables;
+        t.epoch = runs_;
+        cuda_check(launch_phase(t, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s), "box_phase launch");
+      }
+      if (profiling_) event();
+      if (p < K) ce_run_phase_post(p, s);
+    }
+    if (remote_final_writes_) ctx_.barrier(s);
+    return;
+  }
   for (int p = 0; p < n_phases_; ++p) {
     if (!nccl_mode_) ctx_.barrier(s);
     if (profiling_) event();
@@ -1478,6 +1703,20 @@ std::string Program::tasks_json() const {
       o << (g ? "," : "") << "[" << t.targets[g].first << "," << t.targets[g].second << "]";
     o << "]}";
   }
+  // copy-engine relays as pseudo-tasks between the producer chunk (phase k)
+  // and its consumers (phase K+1+k): read the sender's mid box, write the
+  // receiver's relay box
+  for (size_t i = 0; i < ce_copies_.size(); ++i) {
+    const CeCopy& c = ce_copies_[i];
+    if (c.sender != ctx_.rank()) continue;
+    const SliceRegion& b = ce_boxes_[i];
+    o << (first ? "" : ",") << "{\"phase\":" << c.chunk << ".5,\"tensor\":0,\"rank\":" << c.sender
+      << ",\"copy\":1,\"box\":[";
+    first = false;
+    for (size_t d = 0; d < b.bounds.size(); ++d) o << (d ? "," : "") << "[" << b.bounds[d][0] << "," << b.bounds[d][1] << "]";
+    o << "],\"dsts\":[[\"relay\"," << ce_relay_dev_[i] << "," << c.receiver << "]],\"terms\":[[\"mid\","
+      << ce_mid_dev_[i] << "," << c.sender << "]],\"groups\":[],\"wait\":-1,\"need\":0,\"targets\":[]}";
+  }
   o << "]";
   return o.str();
 }
@@ -1496,6 +1735,7 @@ std::string Program::stats_json() const {
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes
     << ",\"kernels_per_run\":" << stats_.kernels_per_run << ",\"streamed\":" << (stats_.streamed ? 1 : 0)
+    << ",\"ce_relay\":" << (stats_.ce_relay ? 1 : 0) << ",\"ce_copies\":" << ce_copies_.size()
     << ",\"trace_off\":" << stats_.trace_off << ",\"trace_ctas\":" << stats_.trace_ctas
     << ",\"phase_items\":[";
   for (size_t i = 0; i < stats_.phase_items.size(); ++i) o << (i ? "," : "") << stats_.phase_items[i];

@@ -133,6 +133,7 @@ struct ProgramStats {
   int64_t src_bytes = 0;     // source-resident bytes on this rank
   int kernels_per_run = 0;   // phase kernels + barrier kernels
   bool streamed = false;     // both plan phases in one launch (ready flags)
+  bool ce_relay = false;     // relays moved by the copy engines
   size_t trace_off = 0;      // EXPERIMENT
   int trace_ctas = 0;
   std::vector<int64_t> phase_items;
@@ -187,6 +188,10 @@ class Program {
   std::vector<BoxTask> spread_shared(std::vector<BoxTask> tasks);
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
   std::vector<BoxTask> stream_phases(const std::vector<BoxTask>& tasks);
+  std::vector<BoxTask> ce_relay(std::vector<BoxTask> tasks);
+  void ce_geometry();  // copy geometry once offsets are assigned
+  void ce_build();     // device-side signal / wait pointer tables
+  void ce_run_phase_post(int p, cudaStream_t s);
   struct Flat;
   Flat flatten(const BoxTask& bt);
   bool tma_capable(const BoxTask& bt);
@@ -211,6 +216,27 @@ class Program {
   bool profiling_ = false;
   bool remote_final_writes_ = false;  // last phase stores into peers' shards
   bool streamed_ = false;             // both plan phases in one launch (ready flags)
+  // HS_PROG_CE_RELAY: phases [0, K) produce row chunk k (exported), K = other
+  // phase-1 work, K+1+k consume chunk k, 2K+1 = other phase-2 work.
+  struct CeCopy {
+    int chunk, sender, receiver;
+    size_t src_off, dst_off;       // arena byte offsets (sender's mid, receiver's relay)
+    size_t width, height, pitch;   // 2-D geometry (bytes, rows, bytes between rows)
+    size_t planes, plane_stride;   // outer dim of a 3-D box
+  };
+  bool ce_mode_ = false;
+  int ce_chunks_ = 4;
+  size_t ce_flag_off_ = 0;                  // symmetric world x K flag words
+  std::vector<CeCopy> ce_copies_;           // every rank's
+  std::vector<SliceRegion> ce_boxes_;       // the logical box of each copy
+  std::vector<DeviceId> ce_mid_dev_, ce_relay_dev_;
+  std::vector<unsigned int**> ce_targets_;  // per chunk: device array of receivers' flag words
+  std::vector<int> ce_ntargets_;
+  std::vector<const unsigned int**> ce_waits_;  // per chunk: device array of my senders' flag words
+  std::vector<int> ce_nwaits_;
+  void* ce_dev_ = nullptr;
+  cudaStream_t ce_stream_ = nullptr;
+  std::vector<cudaEvent_t> ce_events_;
   size_t flag_off_ = 0;               // arena offset of the symmetric ready-flag array
   uint32_t runs_ = 0;                 // run counter = flag epoch
   // HS_PROG_NCCL baseline: per plan phase, this rank's grouped send/recv list

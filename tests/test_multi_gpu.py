@@ -29,7 +29,8 @@ def _gpus():
 # flag sets (HS_PROG_*); "fine:" = streamed programs cut into ~1 KB chunks so
 # the small cases exercise many ready flags per run
 @pytest.mark.parametrize("flags", ["0,14,1", "16,17,32,48", "128,256,480", "512,1024,1152", "2048,2062",
-                                   "4096,4128,8192,12288", "fine:0,32,512,1024,8192"])
+                                   "4096,4128,8192,12288", "fine:0,32,512,1024,8192", "16384,16896",
+                                   "ce3:16384,16896"])
 def test_multi_gpu_parity(tmp_path, flags):
     n = min(_gpus(), 8)
     port = 29517 + sum(map(ord, flags)) % 300
@@ -37,9 +38,11 @@ def test_multi_gpu_parity(tmp_path, flags):
            "--master-addr=127.0.0.1", f"--master-port={port}",
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
     out = os.path.join(tmp_path, "mgpu")
-    env = dict(os.environ, HS_MGPU_OUT=out, HS_MGPU_FLAGS=flags.removeprefix("fine:"))
+    env = dict(os.environ, HS_MGPU_OUT=out, HS_MGPU_FLAGS=flags.split(":")[-1])
     if flags.startswith("fine:"):
         env["HS_STREAM_CHUNK_KB"] = "1"
+    if flags.startswith("ce3:"):  # copy-engine relays in 3 chunks (uneven row cuts)
+        env["HS_CE_CHUNKS"] = "3"
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = []
