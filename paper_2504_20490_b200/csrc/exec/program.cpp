@@ -1407,7 +1407,6 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     const double t0 = std::max(hbm[0] / 6.5e12, nv[0] / 7.7e11), t1 = std::max(hbm[1] / 6.5e12, nv[1] / 7.7e11);
     first_frac[p] = t0 + t1 > 0 ? t0 / (t0 + t1) : 1.0;
     if (const int share = (flags_ >> 16) & 0xff) first_frac[p] = share / 64.0;
-    if (const char* e = std::getenv("HS_STREAM_FIRST_FRAC")) first_frac[p] = std::atof(e);
   }
 
   // TMA item records: header + every operand's first-row address, one
