@@ -148,10 +148,13 @@ enum {
   HS_PROG_PULL_MID = 8192,        /* world > 1: phase 2 pulls remote mid boxes from the
                                      producer's HBM (local groups still fused) instead of
                                      relay stores into the consumer's HBM */
-  HS_PROG_CE_RELAY = 16384        /* world > 1: relays move on the copy engines -- producers
+  HS_PROG_CE_RELAY = 16384,       /* world > 1: relays move on the copy engines -- producers
                                      write their HBM in K row chunks, each chunk is copied to
                                      its consumers by DMA while the SMs continue, consumers of a
                                      chunk wait for it (implies NO_SHARE | PULL_COPIES) */
+  HS_PROG_FANOUT_ONCE = 32768     /* world > 1: a result stored to several destination shards on
+                                     one remote GPU crosses NVLink once; that GPU copies it to
+                                     the others in a following phase */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

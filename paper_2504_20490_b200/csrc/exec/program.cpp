@@ -361,6 +361,8 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     tasks = finish(std::move(tasks));
   }
 
+  if (ctx_.world() > 1 && (flags_ & HS_PROG_FANOUT_ONCE) && !nccl_mode_ && !ce_mode_)
+    tasks = fanout_once(std::move(tasks));
   if (nccl_mode_) stage_for_nccl(tasks);
   if (ce_mode_ && ce_copies_.empty()) ce_mode_ = false;  // no relay to move
 
@@ -949,6 +951,46 @@ std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks) {
     out.push_back(std::move(t));
   }
   return out;
+}
+
+// ---------------------------------------------------------------- fan-out once
+// HS_PROG_FANOUT_ONCE: a last-phase task that stores its result into several
+// destination shards on the same remote rank keeps one of those stores; the
+// remote rank copies that shard's box into the others in a new last phase
+// (streamed like any phase-1 consumer when it applies).  NVLink carries each
+// result once per GPU instead of once per virtual device.
+std::vector<BoxTask> Program::fanout_once(std::vector<BoxTask> tasks) {
+  const int last = n_phases_ - 1;
+  std::vector<BoxTask> copies;
+  for (BoxTask& t : tasks) {
+    if (t.phase != last) continue;
+    std::map<int, std::vector<Operand>> remote;
+    for (const Operand& o : t.dsts) {
+      const int r = loc(o.state, t.tensor, o.dev).rank;
+      if (r != t.rank && o.state == static_cast<int>(final_state_)) remote[r].push_back(o);
+    }
+    std::set<Operand> dropped;
+    for (const auto& [r, os] : remote) {
+      if (os.size() < 2) continue;
+      BoxTask c;
+      c.phase = last + 1;
+      c.kind = t.kind;
+      c.tensor = t.tensor;
+      c.rank = r;
+      c.box = t.box;
+      c.terms = {os[0]};
+      c.dsts.assign(os.begin() + 1, os.end());
+      dropped.insert(os.begin() + 1, os.end());
+      copies.push_back(std::move(c));
+    }
+    if (!dropped.empty())
+      t.dsts.erase(std::remove_if(t.dsts.begin(), t.dsts.end(), [&](const Operand& o) { return dropped.count(o) > 0; }),
+                   t.dsts.end());
+  }
+  if (copies.empty()) return tasks;
+  n_phases_ = last + 2;
+  for (BoxTask& c : copies) tasks.push_back(std::move(c));
+  return tasks;
 }
 
 // ---------------------------------------------------------------- copy-engine relays

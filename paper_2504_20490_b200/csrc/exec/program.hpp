@@ -189,6 +189,7 @@ class Program {
   static std::vector<BoxTask> merge_outputs(std::vector<BoxTask> tasks);
   std::vector<BoxTask> stream_phases(const std::vector<BoxTask>& tasks);
   std::vector<BoxTask> ce_relay(std::vector<BoxTask> tasks);
+  std::vector<BoxTask> fanout_once(std::vector<BoxTask> tasks);
   void ce_geometry();  // copy geometry once offsets are assigned
   void ce_build();     // device-side signal / wait pointer tables
   void ce_run_phase_post(int p, cudaStream_t s);
