@@ -421,7 +421,7 @@ def main():
         achieved = (rd + wr) / kern_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(w.name, dom),
-                "kernel": (f"{'box_phase_tma_kernel' if st['tma_items'] else 'box_phase_kernel'} "
+                "kernel": (f"{('box_phase_tma_static_kernel' if world == 1 else 'box_phase_tma_tail_kernel' if not st.get('streamed') else 'box_phase_tma_kernel') if st['tma_items'] else 'box_phase_kernel'} "
                            f"phase {dom} of {st['phases']} (plan phases {st['plan_phases']}, "
                            f"fused tasks {st['fused_tasks']})"),
                 "bytes_per_launch": rd + wr, "launch_ms": phase_ms[dom],
