@@ -222,3 +222,24 @@ def test_host_buffer_path_pipelined(gpu_ctx):
                 assert np.array_equal(a, want[d])
     finally:
         gpu_ctx.reset(mark)
+
+
+def test_graph_derived_switch_on_gpu(gpu_ctx):
+    """Strategy source -> executor: diff_strategies of a Llama-shaped graph
+    (TP2xPP2 -> TP4 on 4 virtual devices), planned and executed on the B200,
+    every destination shard checked against the counter-hash ground truth."""
+    from paper_2504_20490_b200.executor import Program, ShardLayout
+    from paper_2504_20490_b200.strategy import llama_graph, tp_pp
+    g, n = llama_graph(4, 256, 512, 1024, {"A": tp_pp(2, 2, 4), "B": tp_pp(4, 1, 4)})
+    plan = g.switch_plan(n["A"], n["B"], "bf16")
+    assert len(plan.json()["xfer"]) > 0
+    mark = gpu_ctx.alloc(0)
+    try:
+        lay = ShardLayout(gpu_ctx, plan, 4)
+        lay.fill_src(8, "grid")
+        lay.clear_dst()
+        Program(gpu_ctx, plan, lay).run()
+        gpu_ctx.sync()
+        assert lay.verify_dst(8) == 0
+    finally:
+        gpu_ctx.reset(mark)
