@@ -243,3 +243,69 @@ def test_graph_derived_switch_on_gpu(gpu_ctx):
         assert lay.verify_dst(8) == 0
     finally:
         gpu_ctx.reset(mark)
+
+
+def _random_param_anno(rng, rank):
+    """A random Partial-free annotation on 4 virtual devices (switches move weights)."""
+    devs = [0, 1, 2, 3]
+    rng.shuffle(devs)
+    h = rng.choice([1, 1, 2])
+    sizes = rng.choice([[4], [2], [1]]) if h == 1 else rng.choice([[2, 2], [2, 1], [1, 1]])
+    groups, i = [], 0
+    for s in sizes:
+        groups.append(sorted(devs[i:i + s]))
+        i += s
+    specs = []
+    for g in groups:
+        n = len(g)
+        ent = [] if n == 1 else [(rng.choice([-1] + list(range(rank))), n)]
+        specs.append(ent)
+    hdim = -1 if h == 1 else rng.choice([-1] + list(range(rank)))
+    return H.anno(groups, specs, hdim)
+
+
+def test_switch_round_trip_random_strategies(gpu_ctx):
+    """SPEC acceptance 6: for 20 random strategy pairs over a 3-parameter model,
+    apply_switch(A->B) then (B->A) restores bit-identical shards (every shard
+    checked against the counter-hash ground truth after each leg)."""
+    import random
+    from paper_2504_20490_b200.executor import Program, ShardLayout
+    from paper_2504_20490_b200.graph import Graph
+    rng = random.Random(3)
+    shapes = [(64, 128), (128, 64), (64,)]
+    done = 0
+    for trial in range(60):
+        g = Graph(2)
+        ps = [g.parameter(f"p{i}", list(sh), "bf16") for i, sh in enumerate(shapes)]
+        for s in range(2):
+            for p, sh in zip(ps, shapes):
+                g.annotate(p, s, _random_param_anno(rng, len(sh)))
+        try:
+            ab, ba = g.switch_plan(0, 1, "bf16"), g.switch_plan(1, 0, "bf16")
+        except H.HshardError:  # a random annotation that does not validate on these shapes
+            continue
+        if not ab.json()["xfer"] and not ab.json()["local"]:
+            continue
+        mark = gpu_ctx.alloc(0)
+        try:
+            lay_ab, lay_ba = ShardLayout(gpu_ctx, ab, 4), ShardLayout(gpu_ctx, ba, 4)
+            lay_ab.fill_src(trial, "grid")
+            lay_ab.clear_dst()
+            Program(gpu_ctx, ab, lay_ab).run()
+            gpu_ctx.sync()
+            assert lay_ab.verify_dst(trial) == 0
+            for key in lay_ba.src:  # B -> A starts from the moved shards
+                lay_ba.write("src", key[0], key[1], lay_ab.read("dst", key[0], key[1]))
+            lay_ba.clear_dst()
+            Program(gpu_ctx, ba, lay_ba).run()
+            gpu_ctx.sync()
+            assert lay_ba.verify_dst(trial) == 0
+            for key in lay_ab.src:  # bit-identical to the original A shards
+                assert np.array_equal(lay_ba.read("dst", key[0], key[1]).view(np.uint8),
+                                      lay_ab.read("src", key[0], key[1]).view(np.uint8))
+        finally:
+            gpu_ctx.reset(mark)
+        done += 1
+        if done == 20:
+            break
+    assert done == 20
