@@ -152,9 +152,12 @@ enum {
                                      write their HBM in K row chunks, each chunk is copied to
                                      its consumers by DMA while the SMs continue, consumers of a
                                      chunk wait for it (implies NO_SHARE | PULL_COPIES) */
-  HS_PROG_FANOUT_ONCE = 32768     /* world > 1: a result stored to several destination shards on
+  HS_PROG_FANOUT_ONCE = 32768,    /* world > 1: a result stored to several destination shards on
                                      one remote GPU crosses NVLink once; that GPU copies it to
                                      the others in a following phase */
+  HS_PROG_STATIC_LOCAL = 1 << 24  /* world > 1: launches of local-only items of one task shape
+                                     use the fully static TMA kernel (bits 16..23 hold
+                                     HS_PROG_STREAM_SHARE) */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

@@ -1584,7 +1584,20 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
           // Single GPU: items are uniform local work, a static round-robin is
           // best (no atomic on the producer's critical path).  Multi-GPU: local
           // and NVLink items differ in cost, so the last ~1/16 are dynamic.
-          l.tables.n_static = ctx_.world() == 1
+          // HS_PROG_STATIC_LOCAL: a multi-GPU launch of local-only items of one
+          // task shape is dealt statically too.  Which wins is plan-dependent
+          // (pull-mid cfg2e's producer phase: 80 -> 71 us; cfg5 S3->S4: 8%
+          // slower), so it is a variant the autotuner times.
+          bool uniform_local = (flags_ & HS_PROG_STATIC_LOCAL) != 0;
+          const BoxTask* first = ph[p].src.empty() ? nullptr : ph[p].src.front();
+          for (const BoxTask* bt : ph[p].src) {
+            uniform_local = uniform_local && bt->terms.size() == first->terms.size() &&
+                            bt->dsts.size() == first->dsts.size();
+            for (const auto* ops : {&bt->dsts, &bt->terms})
+              for (const Operand& o : *ops)
+                uniform_local = uniform_local && loc(o.state, bt->tensor, o.dev).rank == bt->rank;
+          }
+          l.tables.n_static = ctx_.world() == 1 || uniform_local
                                   ? cnt
                                   : static_cast<int32_t>((static_cast<int64_t>(cnt) * 15 / 16) / l.grid * l.grid);
         }

@@ -41,6 +41,7 @@ HS_PROG_NO_STREAM = 4096    # world > 1: barrier between plan phases (no per-chu
 HS_PROG_PULL_MID = 8192     # world > 1: pull remote mid boxes (no relay stores), local groups fused
 HS_PROG_CE_RELAY = 16384    # world > 1: relays copied by the copy engines in row chunks, SMs keep computing
 HS_PROG_FANOUT_ONCE = 32768  # world > 1: one NVLink store per remote GPU, local copies to its other shards
+HS_PROG_STATIC_LOCAL = 1 << 24  # world > 1: static dealing for uniform local-only launches
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -314,7 +315,8 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_NO_STREAM, HS_PROG_PULL_MID | HS_PROG_NO_STREAM,
                        HS_PROG_STREAM_SHARE(32), HS_PROG_STREAM_SHARE(51), HS_PROG_FUSE_PHASES,
                        HS_PROG_FANOUT_ONCE, HS_PROG_FANOUT_ONCE | HS_PROG_FUSE_PHASES,
-                       HS_PROG_FANOUT_ONCE | HS_PROG_NO_SHARE]
+                       HS_PROG_FANOUT_ONCE | HS_PROG_NO_SHARE,
+                       HS_PROG_PULL_MID | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL]
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every
 # BASELINE plan at N=2, so it is not a default candidate.
 
