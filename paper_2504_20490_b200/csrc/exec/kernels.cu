@@ -34,9 +34,10 @@ template <>
 struct Arith<uint16_t> {  // bf16 stored as raw bits
   using A = float;
   __device__ static A widen(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
-  __device__ static uint16_t narrow(A f) {
-    const uint32_t u = __float_as_uint(f);
-    return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+  __device__ static uint16_t narrow(A f) {  // round to nearest even: one F2FP instruction
+    uint16_t r;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(f));
+    return r;
   }
   __device__ static A add(A a, A b) { return __fadd_rn(a, b); }
 };
