@@ -161,6 +161,87 @@ __device__ __forceinline__ typename Raw<VB>::type grouped_sum(int nterms, int ng
 }
 
 // Row-0 byte address and row step of an operand for a work item.
+// Packed form for the 16-byte TMA consumers: fp32 pairs in 64-bit registers
+// (FADD2: two IEEE round-to-nearest adds per instruction, the same per-lane
+// result as __fadd_rn), bf16 pairs narrowed by one F2FP.  Same order of
+// additions and roundings as grouped_sum, so bit-identical.
+__device__ __forceinline__ unsigned long long add_f32x2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+template <class T>
+struct Pack2;
+template <>
+struct Pack2<uint16_t> {  // one 32-bit word = 2 bf16 -> 2 fp32 lanes
+  static constexpr int kWordsPerPair = 1;
+  __device__ static unsigned long long widen(const uint32_t* w) {
+    return (static_cast<unsigned long long>(w[0] & 0xffff0000u) << 32) | (w[0] << 16);
+  }
+  __device__ static void narrow(unsigned long long v, uint32_t* w) {
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;"
+        : "=r"(w[0])
+        : "f"(__uint_as_float(static_cast<uint32_t>(v >> 32))), "f"(__uint_as_float(static_cast<uint32_t>(v))));
+  }
+};
+template <>
+struct Pack2<float> {  // two 32-bit words = 2 fp32 lanes
+  static constexpr int kWordsPerPair = 2;
+  __device__ static unsigned long long widen(const uint32_t* w) {
+    return (static_cast<unsigned long long>(w[1]) << 32) | w[0];
+  }
+  __device__ static void narrow(unsigned long long v, uint32_t* w) {
+    w[0] = static_cast<uint32_t>(v);
+    w[1] = static_cast<uint32_t>(v >> 32);
+  }
+};
+
+template <class T, class Get>
+__device__ __forceinline__ uint4 grouped_sum_packed(int nterms, int ngroups, const uint8_t* gsize, Get get) {
+  constexpr int P = 4 / Pack2<T>::kWordsPerPair;  // pairs per 16-byte vector
+  constexpr int WP = Pack2<T>::kWordsPerPair;
+  unsigned long long outer[P], inner[P];
+  int k = 0;
+  const int ng = ngroups ? ngroups : nterms;
+  for (int g = 0; g < ng; ++g) {
+    const int sz = ngroups ? gsize[g] : 1;
+    uint4 x = get(k++);
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(&x);
+#pragma unroll
+    for (int i = 0; i < P; ++i) inner[i] = Pack2<T>::widen(xw + i * WP);
+    for (int j = 1; j < sz; ++j) {
+      x = get(k++);
+#pragma unroll
+      for (int i = 0; i < P; ++i) inner[i] = add_f32x2(inner[i], Pack2<T>::widen(xw + i * WP));
+    }
+    if (sz > 1) {  // the group rounds to the storage type before joining the outer sum
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        uint32_t w[WP];
+        Pack2<T>::narrow(inner[i], w);
+        inner[i] = Pack2<T>::widen(w);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) outer[i] = g == 0 ? inner[i] : add_f32x2(outer[i], inner[i]);
+  }
+  uint4 y;
+  uint32_t* yw = reinterpret_cast<uint32_t*>(&y);
+#pragma unroll
+  for (int i = 0; i < P; ++i) Pack2<T>::narrow(outer[i], yw + i * WP);
+  return y;
+}
+
+// The 16-byte consumers' reduction: packed for bf16 / fp32, generic otherwise.
+template <class T, class Get>
+__device__ __forceinline__ uint4 grouped_sum16(int nterms, int ngroups, const uint8_t* gsize, Get get) {
+  if constexpr (std::is_same_v<T, uint16_t> || std::is_same_v<T, float>)
+    return grouped_sum_packed<T>(nterms, ngroups, gsize, get);
+  else
+    return grouped_sum<T, 16>(nterms, ngroups, gsize, get);
+}
+
 struct RowPtr {
   char* row0;
   int64_t step;
@@ -446,7 +527,7 @@ __device__ __forceinline__ bool tma_consume(const unsigned char* stage, const ui
     } else if (nt == 1) {
       val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
     } else {
-      val = grouped_sum<T, 16>(nt, ng, h->gsize, [&](int k) {
+      val = grouped_sum16<T>(nt, ng, h->gsize, [&](int k) {
         return *reinterpret_cast<const uint4*>(in + (static_cast<size_t>(k) * nvec + v) * 16);
       });
     }
@@ -621,7 +702,7 @@ __device__ __forceinline__ bool tma_consume_tail(const unsigned char* stage, con
     } else if (nt == 1) {
       val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
     } else {
-      val = grouped_sum<T, 16>(nt, ng, h->gsize, [&](int k) {
+      val = grouped_sum16<T>(nt, ng, h->gsize, [&](int k) {
         return *reinterpret_cast<const uint4*>(in + (static_cast<size_t>(k) * nvec + v) * 16);
       });
     }
@@ -782,7 +863,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
       } else if (nt == 1) {
         val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
       } else {
-        val = grouped_sum<T, 16>(nt, ng, h->gsize, [&](int k) {
+        val = grouped_sum16<T>(nt, ng, h->gsize, [&](int k) {
           return *reinterpret_cast<const uint4*>(in + (static_cast<size_t>(k) * nvec + v) * 16);
         });
       }
