@@ -180,6 +180,8 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
       covered(src, t, m, task.box, why);
       task.terms.push_back({src, m});
     }
+    // Zero-width top-tier slices give empty boxes: no work.
+    if (cells_of(task.box) == 0) return;
     tasks.push_back(std::move(task));
   };
   auto region_of = [this](int state, DeviceId d) { return loc(state, 0, d).region; };

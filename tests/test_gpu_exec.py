@@ -81,6 +81,30 @@ def test_random_plans_bit_exact(gpu_ctx, dtype):
     assert len(kinds) >= 8, kinds
 
 
+def test_zero_width_top_tier_slices(gpu_ctx):
+    """validate accepts top-tier ratio slices that floor to zero
+    width (annotation.cpp:304-318); the reference's Tensor::slice then throws
+    (tensor.cpp:55-57).  Here an empty box is simply no work: the devices of a
+    zero-width subgroup hold empty shards and every other shard must still be
+    bit-identical to the oracle."""
+    rng = random.Random(33)
+    done = tries = 0
+    while done < 40 and tries < 20000:
+        tries += 1
+        src, dst, shape = rand_pair(rng)
+        shape = [rng.choice([1, 2, 3, 4, 6]) if rng.random() < 0.7 else x for x in shape]
+        if not (zero_width(src, shape) or zero_width(dst, shape)):
+            continue
+        try:
+            plan = H.classify(src, dst, shape, "f32")
+            ox.execute_plan(plan.json(), ox.scatter(src, shape, "f32", 1), "f32")
+        except (H.HshardError, ox.OracleError):
+            continue
+        _gpu_case(gpu_ctx, plan, src, dst, shape, "f32", rng.randrange(1 << 30), "grid")
+        done += 1
+    assert done >= 20, done
+
+
 def test_appendix_b1_rejected_on_compile(gpu_ctx):
     from paper_2504_20490_b200.executor import Program, ShardLayout
     src, dst = "hsize=1 hdim=-1 [(3,5,2,7){1:4}]", "hsize=1 hdim=-1 [(3,5,2,7){-1:2,1:2}]"

@@ -123,6 +123,38 @@ def _partition_or_unsupported(w, plan, world, flags):
     check_partition(w, plan, per_rank, world)
 
 
+def test_zero_width_slices_partition():
+    """top-tier ratio slices that floor to zero width compile
+    (empty boxes are dropped -- they once divided by a zero extent) and still
+    tile every destination shard, on 1, 2 and 5 ranks and across variants."""
+    import random
+    from types import SimpleNamespace
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from gen_cases import rand_pair, zero_width
+    rng = random.Random(33)
+    done = tries = 0
+    while done < 40 and tries < 20000:
+        tries += 1
+        s, d, sh = rand_pair(rng)
+        sh = [rng.choice([1, 2, 3, 4, 6]) if rng.random() < 0.7 else x for x in sh]
+        if not (zero_width(s, sh) or zero_width(d, sh)):
+            continue
+        try:
+            plan = H.classify(s, d, sh, "f32")
+        except H.HshardError:
+            continue
+        w = SimpleNamespace(name=f"zero-width {s} -> {d} {sh}", n_virtual=10)
+        try:
+            for world in (1, 2, 5):
+                for flags in (0, 14, 8192, 32768):
+                    _partition_or_unsupported(w, plan, world, flags)
+        except H.HshardError as e:
+            assert e.code == "UnexecutableStep", e  # Appendix-B1 plans, as without zero widths
+            continue
+        done += 1
+    assert done >= 30, done
+
+
 @pytest.mark.parametrize("world", [4, 8])
 def test_partitioning_in_process(world):
     for name in NAMES:
