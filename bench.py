@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--sweep", default=None,
                     help="comma list of workloads (or 'all'): one JSON line per workload instead "
                          "of the headline line")
-    ap.add_argument("--no-tune", action="store_true", help="world > 1: no autotuning of the program variant")
+    ap.add_argument("--no-tune", action="store_true", help="no autotuning of the program variant")
     ap.add_argument("--flags", type=int, default=0,
                     help="HS_PROG_* bits: 1 fuse, 2 no-fuse, 4 no-TMA, 8 no-merge (14 = plain baseline)")
     return ap.parse_args()
@@ -291,12 +291,14 @@ def main():
         else:
             plan = H.plan_switch(work.transitions, work.dtype)
         lay = ShardLayout(ctx, plan, work.n_virtual)
-        if world > 1 and args.flags == 0 and not args.no_tune:
-            # cross-rank rewrite variants are chosen by timing them (untimed warm-up)
+        if args.flags == 0 and not args.no_tune:
+            # program variants (cross-rank rewrites; at N=1 the copy store path) are chosen
+            # by timing them (untimed warm-up)
             lay.fill_src(1, "grid", sp)
             stream.synchronize()
             prog, tuned = autotune(ctx, plan, lay, stream=stream,
-                                   steps=3 if W.resident_bytes(work) > 20e9 else 10)
+                                   steps=3 if W.resident_bytes(work) > 20e9 else
+                                   10 if W.resident_bytes(work) > 2e9 else 50)
             tune_log[work.name] = {"chosen_flags": prog_flags(prog, tuned), "ms_by_flags": tuned}
         else:
             prog = Program(ctx, plan, lay, args.flags)

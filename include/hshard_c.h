@@ -155,9 +155,13 @@ enum {
   HS_PROG_FANOUT_ONCE = 32768,    /* world > 1: a result stored to several destination shards on
                                      one remote GPU crosses NVLink once; that GPU copies it to
                                      the others in a following phase */
-  HS_PROG_STATIC_LOCAL = 1 << 24  /* world > 1: launches of local-only items of one task shape
+  HS_PROG_STATIC_LOCAL = 1 << 24, /* world > 1: launches of local-only items of one task shape
                                      use the fully static TMA kernel (bits 16..23 hold
                                      HS_PROG_STREAM_SHARE) */
+  HS_PROG_BULK_STORE = 1 << 25    /* the static TMA kernel stores the first two outputs of a copy
+                                     with TMA bulk stores out of the staging buffer (the rest from
+                                     registers); faster on some plans, slower on others -- the
+                                     autotuner times it */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

@@ -407,6 +407,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// TMA bulk store shared -> global, tracked by the issuing thread's bulk groups.
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory source of every committed group has been read
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// ... of every committed group but the most recent one
+__device__ __forceinline__ void bulk_wait_read_but_last() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Streamed launches, signalling side.  A system-scope fence in an SM that is
 // streaming costs microseconds (it waits for the SM's outstanding memory
 // traffic), so consumer warps never issue one: each consumer warp of an item
@@ -793,7 +810,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
 // Single-GPU variant (items dealt round-robin, no scheduler state): the
 // kernel measured at 93% of HBM peak on cfg2e; kept verbatim because the
 // dynamic-schedule kernel's extra per-item work costs ~8% there.
-template <class T>
+// kBulk (HS_PROG_BULK_STORE): copies leave through TMA bulk stores.  A template
+// parameter, so the default instantiation's reduce path compiles exactly as
+// before (a runtime branch here cost cfg2b/cfg2d 13-17%).
+template <class T, bool kBulk>
 __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(PhaseTables t) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* stage = smem;
@@ -845,6 +865,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
   const int ctid = threadIdx.x - 32;
   constexpr int nct = kTmaThreads - 32;
   int iter = 0;
+  int held = -1;  // warp 1: the stage its last bulk stores may still be reading
   for (int it = blockIdx.x; it < t.n_items; it += gridDim.x, ++iter) {
     const int s = iter % kTmaStages;
     mbar_wait(&full[s], (iter / kTmaStages) & 1);
@@ -854,6 +875,51 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     const int ng = h->ngroups;
     const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;
     const unsigned char* in = stage + s * kStageBytes;
+    if (kBulk && nt == 1) {
+      // A copy: the staged rows of the first nb outputs leave through TMA
+      // bulk stores, one (output, row) per lane of the first consumer warp;
+      // all consumer warps store the remaining outputs from registers, so
+      // fan-out copies keep both store paths busy and the TMA unit is not
+      // monopolised by stores while it must also feed the stages.  The first
+      // warp releases a stage one copy later, once the stores have read it,
+      // so the store queue never drains between items.
+      const int nb = min(no, t.bulk_store);
+      if (warp == 1) {
+        const int nrow = h->nrow;
+        const uint32_t row_bytes = static_cast<uint32_t>(nvcol) * 16;
+        for (int j = lane; j < nb * nrow; j += 32) {
+          const int o = j / nrow, r = j - o * nrow;
+          bulk_s2g(outs[o].row0 + r * outs[o].step, smem_u32(in) + r * row_bytes, row_bytes);
+        }
+        bulk_commit();
+      }
+      if (no > nb)
+        for (int v = ctid; v < nvec; v += nct) {
+          const int r = v / nvcol;
+          const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
+          const uint4 val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
+          for (int o = nb; o < no; ++o)
+            __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
+        }
+      if (warp == 1) {
+        if (held >= 0) {
+          bulk_wait_read_but_last();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[held]);
+        }
+        held = s;
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      continue;
+    }
+    if (kBulk && warp == 1 && held >= 0) {  // a non-copy item: release the held stage first
+      bulk_wait_read_all();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[held]);
+      held = -1;
+    }
     for (int v = ctid; v < nvec; v += nct) {
       const int r = v / nvcol;
       const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
@@ -872,6 +938,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  if (kBulk && warp == 1) bulk_wait_all();  // stores complete before the CTA retires
 }
 
 // ---------------------------------------------------------------- datagen
@@ -1076,8 +1143,10 @@ struct PhaseK {
       static bool configured = [] {
         cudaFuncSetAttribute(box_phase_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kDynSmem));
-        cudaFuncSetAttribute(box_phase_tma_static_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kTmaSmem));
+        cudaFuncSetAttribute(box_phase_tma_static_kernel<T, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
+        cudaFuncSetAttribute(box_phase_tma_static_kernel<T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
         cudaFuncSetAttribute(box_phase_tma_tail_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kTmaSmem));
         return true;
@@ -1086,7 +1155,10 @@ struct PhaseK {
       if (t.sigs)  // streamed: ready flags, two queues, signaller warp
         box_phase_tma_kernel<T><<<g, dim3(kDynThreads), kDynSmem, s>>>(t);
       else if (t.n_static >= t.n_items)
-        box_phase_tma_static_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+        if (t.bulk_store)
+          box_phase_tma_static_kernel<T, true><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+        else
+          box_phase_tma_static_kernel<T, false><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       else
         box_phase_tma_tail_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       return;

@@ -100,6 +100,8 @@ struct PhaseTables {
   const unsigned int* wait_flags;    // this rank's flags
   int* error;                        // set when a wait times out (DeadlockDetected)
   unsigned long long* trace;         // debug (HS_TRACE): 8 globaltimer words per CTA, or null
+  int32_t bulk_store;                // static TMA kernel: a copy's first bulk_store outputs leave
+                                     // through TMA bulk stores (0: all from registers)
 };
 
 // Shared-memory staging of the TMA kernel: kStages ring buffers of

@@ -41,6 +41,9 @@ constexpr int64_t kItemBytes = 64 * 1024;     // register path, output bytes per
 constexpr int64_t kTmaItemBytes = 32 * 1024;  // TMA path upper bound (also <= stage / nterms)
 constexpr int kBlocksPerSm = 2;
 constexpr int kSlots = 9;
+// HS_PROG_BULK_STORE: a copy's outputs stored by TMA bulk stores (the rest from
+// registers, so the TMA unit still has room for the loads feeding the stages)
+constexpr int kBulkStoreOutputs = 2;
 
 SliceRegion bounds_only(const SliceRegion& r) {
   SliceRegion b;
@@ -1562,6 +1565,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables.n_first = cnt;
       l.tables.first_ctas = l.grid;
       l.tables.error = ctx_.error_flag();
+      l.tables.bulk_store = (flags_ & HS_PROG_BULK_STORE) ? kBulkStoreOutputs : 0;
       if (l.tma && std::getenv("HS_TRACE") && !ctx_.is_analysis()) {
         stats_.trace_off = ctx_.alloc(static_cast<size_t>(l.grid) * 64);
         stats_.trace_ctas = l.grid;

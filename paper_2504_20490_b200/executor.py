@@ -42,6 +42,7 @@ HS_PROG_PULL_MID = 8192     # world > 1: pull remote mid boxes (no relay stores)
 HS_PROG_CE_RELAY = 16384    # world > 1: relays copied by the copy engines in row chunks, SMs keep computing
 HS_PROG_FANOUT_ONCE = 32768  # world > 1: one NVLink store per remote GPU, local copies to its other shards
 HS_PROG_STATIC_LOCAL = 1 << 24  # world > 1: static dealing for uniform local-only launches
+HS_PROG_BULK_STORE = 1 << 25  # static TMA kernel: copies' first two outputs leave through TMA bulk stores
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -317,6 +318,8 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_FANOUT_ONCE, HS_PROG_FANOUT_ONCE | HS_PROG_FUSE_PHASES,
                        HS_PROG_FANOUT_ONCE | HS_PROG_NO_SHARE,
                        HS_PROG_PULL_MID | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL]
+AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE]
+TUNE_MARGIN = 0.01  # a later candidate must beat the best so far by 1% (timing noise)
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every
 # BASELINE plan at N=2, so it is not a default candidate.
 
@@ -327,14 +330,19 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
 
     Every candidate is compiled and timed for `steps` runs with CUDA events on `stream`; the
     max over ranks decides (all ranks take the same choice).  Results are bit-identical across
-    variants -- only the placement of work between ranks differs.  world == 1 has nothing to
-    tune.  Returns (program, {flags: ms}).
+    variants -- only the placement of work between ranks, or the store path, differs.  At
+    world == 1 the only variant is HS_PROG_BULK_STORE, for plans with copy tasks.
+    Returns (program, {flags: ms}).
     """
-    if ctx.world == 1:
-        return Program(ctx, plan, layout, 0), {}
     import torch
     import torch.distributed as dist
-    cands = list(candidates if candidates is not None else AUTOTUNE_CANDIDATES)
+    if ctx.world == 1:
+        prog = Program(ctx, plan, layout, 0)
+        if candidates is None and prog.stats()["copy_tasks"] == 0:
+            return prog, {}
+        prog.close()
+    cands = list(candidates if candidates is not None else
+                 AUTOTUNE_CANDIDATES if ctx.world > 1 else AUTOTUNE_CANDIDATES_1GPU)
     s = stream if stream is not None else torch.cuda.current_stream()
     sp = s.cuda_stream
     best, best_ms, timings = None, None, {}
@@ -352,7 +360,8 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
             prog.run(sp)
         s.synchronize()
         ctx.sync()
-        dist.barrier(group=group)
+        if ctx.world > 1:
+            dist.barrier(group=group)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(s):
             a.record()
@@ -362,10 +371,11 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
         b.synchronize()
         ctx.sync()
         t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        if ctx.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         ms = float(t.item())
         timings[flags] = ms
-        if best is None or ms < best_ms:
+        if best is None or ms < best_ms * (1 - TUNE_MARGIN):
             if best is not None:
                 best.close()
             best, best_ms = prog, ms

@@ -26,7 +26,8 @@ from paper_2504_20490_b200 import workloads as W
 pytestmark = pytest.mark.gpu
 
 
-FLAG_SETS = [0, 2 | 4 | 8]  # default (fused, TMA, merged outputs) and the plain register path
+# default (fused, TMA, merged outputs), the plain register path, TMA bulk stores for copies
+FLAG_SETS = [0, 2 | 4 | 8, 1 << 25]
 
 
 def _gpu_case(ctx, plan, src, dst, shape, dtype, seed, mode, n_virtual=10, flag_sets=FLAG_SETS):
@@ -135,17 +136,20 @@ def test_switch_random_bit_exact(gpu_ctx):
         mark = gpu_ctx.alloc(0)
         lay = ShardLayout(gpu_ctx, plan, 10)
         lay.fill_src(it, "real")
-        lay.clear_dst()
         src = {}
         for slot, (tid, s, d, shp) in enumerate(entries):
             for dev, a in ox.scatter(s, shp, "bf16", it, tid, "real").items():
                 src[(tid, dev)] = a
-        Program(gpu_ctx, plan, lay).run()
-        gpu_ctx.sync()
         want = ox.execute_switch(plan.json(), entries, src, "bf16")
-        for (slot, dev) in lay.dst:
-            tid = entries[slot][0]
-            assert np.array_equal(lay.read("dst", slot, dev), want[(tid, dev)]), (it, slot, dev)
+        for flags in (0, 1 << 25):  # default and TMA bulk stores
+            lay.clear_dst()
+            prog = Program(gpu_ctx, plan, lay, flags)
+            prog.run()
+            gpu_ctx.sync()
+            for (slot, dev) in lay.dst:
+                tid = entries[slot][0]
+                assert np.array_equal(lay.read("dst", slot, dev), want[(tid, dev)]), (it, flags, slot, dev)
+            prog.close()
         gpu_ctx.reset(mark)
 
 
@@ -188,11 +192,13 @@ def test_switch_full_size_properties(gpu_ctx, name):
     try:
         lay = ShardLayout(gpu_ctx, plan, w.n_virtual)
         lay.fill_src(5, "grid")
-        lay.clear_dst()
-        prog = Program(gpu_ctx, plan, lay)
-        prog.run()
-        gpu_ctx.sync()
-        assert lay.verify_dst(5) == 0
+        for flags in (0, 1 << 25):  # default and TMA bulk stores
+            lay.clear_dst()
+            prog = Program(gpu_ctx, plan, lay, flags)
+            prog.run()
+            gpu_ctx.sync()
+            assert lay.verify_dst(5) == 0, flags
+            prog.close()
     finally:
         gpu_ctx.reset(mark)
 

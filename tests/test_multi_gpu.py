@@ -30,7 +30,9 @@ def _gpus():
 # the small cases exercise many ready flags per run
 @pytest.mark.parametrize("flags", ["0,14,1", "16,17,32,48", "128,256,480", "512,1024,1152", "2048,2062",
                                    "4096,4128,8192,12288", "fine:0,32,512,1024,8192", "16384,16896",
-                                   "ce3:16384,16896", "32768,32769,32896"])
+                                   "ce3:16384,16896", "32768,32769,32896",
+                                   # STATIC_LOCAL | PULL_MID | NO_STREAM, without / with BULK_STORE
+                                   "16789504,50343936"])
 def test_multi_gpu_parity(tmp_path, flags):
     n = min(_gpus(), 8)
     port = 29517 + sum(map(ord, flags)) % 300
