@@ -264,9 +264,14 @@ def main():
     from paper_2504_20490_b200 import hshard as H
     from paper_2504_20490_b200.executor import Context, Program, ShardLayout, autotune
 
+    # Validation aid only: HS_ARENA_GB with more ranks than GPUs runs e.g. the N=8
+    # flow on a 4-GPU box (two ranks per GPU); its timings mean nothing.
+    local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     free, _ = torch.cuda.mem_get_info(local)
     arena = max(8 << 30, free - (10 << 30))
+    if os.environ.get("HS_ARENA_GB"):
+        arena = int(float(os.environ["HS_ARENA_GB"]) * (1 << 30))
     ctx = Context(arena, rank=rank, world=world, gpu=local)
     if world > 1 and args.flags & 2048:
         ctx.init_nccl()

@@ -26,7 +26,9 @@ def main():
     from paper_2504_20490_b200.executor import Context, Program, ShardLayout
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # HS_TEST_RANKS may oversubscribe the GPUs (8 ranks on a 4-GPU box, two per
+    # GPU) to exercise 8-rank IPC, barriers and partitions where only 4 GPUs exist
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     ctx = Context(8 << 30, rank=rank, world=world, gpu=local)

@@ -34,7 +34,7 @@ def _gpus():
                                    # STATIC_LOCAL | PULL_MID | NO_STREAM, without / with BULK_STORE
                                    "16789504,50343936"])
 def test_multi_gpu_parity(tmp_path, flags):
-    n = min(_gpus(), 8)
+    n = int(os.environ.get("HS_TEST_RANKS", min(_gpus(), 8)))  # > GPUs: ranks share GPUs
     port = 29517 + sum(map(ord, flags)) % 300
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
