@@ -158,10 +158,13 @@ enum {
   HS_PROG_STATIC_LOCAL = 1 << 24, /* world > 1: launches of local-only items of one task shape
                                      use the fully static TMA kernel (bits 16..23 hold
                                      HS_PROG_STREAM_SHARE) */
-  HS_PROG_BULK_STORE = 1 << 25    /* the static TMA kernel stores the first two outputs of a copy
+  HS_PROG_BULK_STORE = 1 << 25,   /* the static TMA kernel stores the first two outputs of a copy
                                      with TMA bulk stores out of the staging buffer (the rest from
                                      registers); faster on some plans, slower on others -- the
                                      autotuner times it */
+  HS_PROG_SEPARATE_BARRIERS = 1 << 26 /* world > 1: every cross-rank barrier is its own launch
+                                     (default: folded into the prologue of the phase's first TMA
+                                     kernel where that is a static / tail TMA launch) */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */
@@ -215,6 +218,12 @@ int hs_verify_shard(hs_ctx* ctx, const char* anno, const int64_t* shape, int ndi
 int hs_ctx_read(hs_ctx* ctx, size_t offset, void* host, size_t bytes);
 int hs_ctx_write(hs_ctx* ctx, size_t offset, const void* host, size_t bytes);
 int hs_ctx_sync(hs_ctx* ctx);
+/* Enqueue a device-side cross-rank barrier on `stream` (NULL = the context's
+ * stream): after it, every rank's work enqueued before its own barrier call
+ * is complete and visible (the barrier each program run opens with).  Every
+ * rank must call it; a rank that never arrives is reported as
+ * DeadlockDetected by hs_ctx_sync.  No-op at world 1. */
+int hs_ctx_barrier(hs_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

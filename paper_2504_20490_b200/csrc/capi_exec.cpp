@@ -223,4 +223,8 @@ int hs_ctx_sync(hs_ctx* ctx) {
   });
 }
 
+int hs_ctx_barrier(hs_ctx* ctx, void* stream) {
+  return guarded([&] { ctx->c->barrier(stream ? static_cast<cudaStream_t>(stream) : ctx->c->stream()); });
+}
+
 }  // extern "C"

@@ -491,6 +491,35 @@ __device__ void tma_signaller(const PhaseTables& t, SigRing* ring, int lane) {
 // Streamed launches: the producer warp's lane 0 waits until a consumer
 // piece's producers have all signalled this run; bounded by ~10 s, after
 // which it records DeadlockDetected and proceeds (never a hang).
+// Folded barrier, thread 0 of every CTA: CTA 0 announces this rank (stream
+// order: everything enqueued before this kernel has completed), then each CTA
+// waits until every rank has announced -- launch_barrier's protocol without
+// its launch.  False on timeout (error recorded; the CTA then does no work).
+__device__ __noinline__ bool folded_barrier(unsigned int* const* flags, int world, int rank,
+                                            unsigned int epoch, int* error) {
+  if (blockIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags[p] + rank), "r"(epoch) : "memory");
+  }
+  const unsigned int* mine = flags[rank];
+  const unsigned long long t0 = global_ns();
+  for (int p = 0; p < world; ++p) {
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + p) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      if (global_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
+        *error = 1;
+        return false;
+      }
+    }
+  }
+  // the TMA (async proxy) loads that follow read what peers wrote
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  return true;
+}
+
 __device__ __forceinline__ void tma_wait(const PhaseTables& t, int flag, int need) {
   const unsigned int want = t.epoch * static_cast<unsigned int>(need);
   const unsigned int* f = t.wait_flags + flag;
@@ -746,6 +775,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (t.bar_flags) {  // folded cross-rank barrier (replaces a barrier launch)
+    volatile int* ok = reinterpret_cast<volatile int*>(meta);  // unused until the first item
+    if (threadIdx.x == 0) *ok = folded_barrier(t.bar_flags, t.bar_world, t.bar_rank, t.bar_epoch, t.error);
+    __syncthreads();
+    const int good = *ok;
+    __syncthreads();  // every thread has read it before the producer reuses meta
+    if (!good) return;
+  }
   const int W = t.rec_words;
 
   if (warp == 0) {
@@ -829,6 +866,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (t.bar_flags) {  // folded cross-rank barrier (replaces a barrier launch)
+    volatile int* ok = reinterpret_cast<volatile int*>(meta);  // unused until the first item
+    if (threadIdx.x == 0) *ok = folded_barrier(t.bar_flags, t.bar_world, t.bar_rank, t.bar_epoch, t.error);
+    __syncthreads();
+    const int good = *ok;
+    __syncthreads();  // every thread has read it before the producer reuses meta
+    if (!good) return;
+  }
   const int W = t.rec_words;
 
   if (warp == 0) {

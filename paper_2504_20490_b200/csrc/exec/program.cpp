@@ -1611,10 +1611,17 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       d.launches.push_back(l);
       ++launches;
     }
+    // The phase's opening barrier runs in the prologue of its first launch
+    // when that is a static / tail TMA kernel (not the streamed kernel, not
+    // the register path): one launch and its gap fewer per barrier.
+    d.fold_barrier = ctx_.world() > 1 && !nccl_mode_ && !ce_mode_ && !(flags_ & HS_PROG_SEPARATE_BARRIERS) &&
+                     !d.launches.empty() && d.launches[0].tma && !d.launches[0].tables.sigs &&
+                     d.launches[0].tables.n_first >= d.launches[0].tables.n_items;
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }
-  const int barriers = ctx_.world() > 1 && !nccl_mode_ ? n_phases_ + (remote_final_writes_ ? 1 : 0) : 0;
+  int barriers = ctx_.world() > 1 && !nccl_mode_ ? n_phases_ + (remote_final_writes_ ? 1 : 0) : 0;
+  for (const DevicePhase& d : dphases_) barriers -= d.fold_barrier ? 1 : 0;
   stats_.kernels_per_run = launches + barriers;
 }
 
@@ -1660,11 +1667,20 @@ void Program::run(cudaStream_t s) {
     return;
   }
   for (int p = 0; p < n_phases_; ++p) {
-    if (!nccl_mode_) ctx_.barrier(s);
+    const bool fold = dphases_[p].fold_barrier;
+    const unsigned int bar_epoch = fold ? ctx_.next_epoch() : 0;
+    if (!nccl_mode_ && !fold) ctx_.barrier(s);
     if (profiling_) event();
-    for (const Launch& l : dphases_[p].launches) {
+    for (size_t i = 0; i < dphases_[p].launches.size(); ++i) {
+      const Launch& l = dphases_[p].launches[i];
       PhaseTables t = l.tables;
       t.epoch = runs_;
+      if (fold && i == 0) {
+        t.bar_flags = ctx_.peer_flag_table();
+        t.bar_world = ctx_.world();
+        t.bar_rank = ctx_.rank();
+        t.bar_epoch = bar_epoch;
+      }
       cuda_check(launch_phase(t, dtype_, l.vec_bytes, l.tma, l.reduce, l.grid, s), "box_phase launch");
     }
     if (nccl_mode_ && p % 2 == 0 && !exchanges_[p / 2].empty()) {

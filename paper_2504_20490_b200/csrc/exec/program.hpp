@@ -49,6 +49,10 @@ class Context {
 
   // Cross-rank barrier on `s` (no-op when world == 1).
   void barrier(cudaStream_t s);
+  // The same barrier folded into the prologue of the kernel launched next:
+  // consumes an epoch; the kernel signals and waits (PhaseTables::bar_*).
+  unsigned int next_epoch() { return ++epoch_; }
+  unsigned int* const* peer_flag_table() const { return d_peer_flags_; }
   void check_barrier_error();
 
   unsigned long long* scratch_counter() const { return counter_; }
@@ -174,6 +178,7 @@ class Program {
   };
   struct DevicePhase {
     std::vector<Launch> launches;  // TMA launch + one per vector width present
+    bool fold_barrier = false;     // the opening barrier runs in launches[0]'s prologue
   };
 
   void lower(const CommPlan* comm, const SwitchPlan* sw);

@@ -43,6 +43,7 @@ HS_PROG_CE_RELAY = 16384    # world > 1: relays copied by the copy engines in ro
 HS_PROG_FANOUT_ONCE = 32768  # world > 1: one NVLink store per remote GPU, local copies to its other shards
 HS_PROG_STATIC_LOCAL = 1 << 24  # world > 1: static dealing for uniform local-only launches
 HS_PROG_BULK_STORE = 1 << 25  # static TMA kernel: copies' first two outputs leave through TMA bulk stores
+HS_PROG_SEPARATE_BARRIERS = 1 << 26  # world > 1: barriers as their own launches, not kernel prologues
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -124,6 +125,10 @@ class Context:
 
     def sync(self) -> None:
         check(LIB.hs_ctx_sync(self._h))
+
+    def barrier(self, stream=None) -> None:
+        """Device-side cross-rank barrier enqueued on `stream` (a cuda stream handle; None = ctx stream)."""
+        check(LIB.hs_ctx_barrier(self._h, c_void_p(stream or 0)))
 
     def close(self) -> None:
         h, self._h = getattr(self, "_h", None), None

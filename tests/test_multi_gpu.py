@@ -32,7 +32,9 @@ def _gpus():
                                    "4096,4128,8192,12288", "fine:0,32,512,1024,8192", "16384,16896",
                                    "ce3:16384,16896", "32768,32769,32896",
                                    # STATIC_LOCAL | PULL_MID | NO_STREAM, without / with BULK_STORE
-                                   "16789504,50343936"])
+                                   "16789504,50343936",
+                                   # barriers as separate launches (default: folded into kernels)
+                                   "67108864,67121152"])
 def test_multi_gpu_parity(tmp_path, flags):
     n = int(os.environ.get("HS_TEST_RANKS", min(_gpus(), 8)))  # > GPUs: ranks share GPUs
     port = 29517 + sum(map(ord, flags)) % 300
