@@ -163,8 +163,8 @@ enum {
                                      registers); faster on some plans, slower on others -- the
                                      autotuner times it */
   HS_PROG_SEPARATE_BARRIERS = 1 << 26 /* world > 1: every cross-rank barrier is its own launch
-                                     (default: folded into the prologue of the phase's first TMA
-                                     kernel where that is a static / tail TMA launch) */
+                                     (default: folded into the prologue of the phase's first
+                                     launch when that is a TMA kernel) */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

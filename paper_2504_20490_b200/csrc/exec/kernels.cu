@@ -607,6 +607,14 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (t.bar_flags) {  // folded cross-rank barrier (replaces a barrier launch)
+    volatile int* ok = reinterpret_cast<volatile int*>(meta);  // unused until the first item
+    if (threadIdx.x == 0) *ok = folded_barrier(t.bar_flags, t.bar_world, t.bar_rank, t.bar_epoch, t.error);
+    __syncthreads();
+    const int good = *ok;
+    __syncthreads();  // every thread has read it before the producer reuses meta
+    if (!good) return;
+  }
   const int W = t.rec_words;
 
   if (warp == kConsumerWarps + 1) {  // ---- signaller warp

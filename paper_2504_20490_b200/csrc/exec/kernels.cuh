@@ -102,7 +102,7 @@ struct PhaseTables {
   unsigned long long* trace;         // debug (HS_TRACE): 8 globaltimer words per CTA, or null
   int32_t bulk_store;                // static TMA kernel: a copy's first bulk_store outputs leave
                                      // through TMA bulk stores (0: all from registers)
-  // Folded cross-rank barrier (static / tail TMA kernels): when bar_flags is
+  // Folded cross-rank barrier (TMA kernels): when bar_flags is
   // set the kernel opens with launch_barrier's protocol for bar_epoch instead
   // of a separate barrier launch in front of it.
   unsigned int* const* bar_flags;    // every rank's flag array (peer-mapped), or null

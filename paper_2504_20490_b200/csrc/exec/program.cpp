@@ -1612,11 +1612,10 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       ++launches;
     }
     // The phase's opening barrier runs in the prologue of its first launch
-    // when that is a static / tail TMA kernel (not the streamed kernel, not
-    // the register path): one launch and its gap fewer per barrier.
+    // when that is a TMA kernel (not the register path): one launch and its
+    // gap fewer per barrier.
     d.fold_barrier = ctx_.world() > 1 && !nccl_mode_ && !ce_mode_ && !(flags_ & HS_PROG_SEPARATE_BARRIERS) &&
-                     !d.launches.empty() && d.launches[0].tma && !d.launches[0].tables.sigs &&
-                     d.launches[0].tables.n_first >= d.launches[0].tables.n_items;
+                     !d.launches.empty() && d.launches[0].tma;
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }
