@@ -732,9 +732,10 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
 // One consumer-warp pass over pipeline stage `iter`: wait for it, form every
 // output vector of the item from shared memory, release the stage.  Returns
 // false on the producer's end marker.
-template <class T>
+template <class T, bool kBulk>
 __device__ __forceinline__ bool tma_consume_tail(const unsigned char* stage, const uint4* meta,
-                                            uint64_t* full, uint64_t* empty, int iter, int lane) {
+                                            uint64_t* full, uint64_t* empty, int iter, int lane,
+                                            int bulk_outs, int& held) {
   const int ctid = threadIdx.x - 32;
   constexpr int nct = kTmaThreads - 32;
   const int s = iter % kTmaStages;
@@ -747,6 +748,47 @@ __device__ __forceinline__ bool tma_consume_tail(const unsigned char* stage, con
   const int ng = h->ngroups;
   const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;
   const unsigned char* in = stage + s * kStageBytes;
+  if constexpr (kBulk) {
+    const int warp = threadIdx.x >> 5;
+    if (nt == 1) {  // as in box_phase_tma_static_kernel: outputs may be peer addresses
+      const int nb = min(no, bulk_outs);
+      if (warp == 1) {
+        const int nrow = h->nrow;
+        const uint32_t row_bytes = static_cast<uint32_t>(nvcol) * 16;
+        for (int j = lane; j < nb * nrow; j += 32) {
+          const int o = j / nrow, r = j - o * nrow;
+          bulk_s2g(outs[o].row0 + r * outs[o].step, smem_u32(in) + r * row_bytes, row_bytes);
+        }
+        bulk_commit();
+      }
+      if (no > nb)
+        for (int v = ctid; v < nvec; v += nct) {
+          const int r = v / nvcol;
+          const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
+          const uint4 val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
+          for (int o = nb; o < no; ++o)
+            __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
+        }
+      if (warp == 1) {
+        if (held >= 0) {
+          bulk_wait_read_but_last();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[held]);
+        }
+        held = s;
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      return true;
+    }
+    if (warp == 1 && held >= 0) {  // a non-copy item: release the held stage first
+      bulk_wait_read_all();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[held]);
+      held = -1;
+    }
+  }
   for (int v = ctid; v < nvec; v += nct) {
     const int r = v / nvcol;
     const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
@@ -767,7 +809,7 @@ __device__ __forceinline__ bool tma_consume_tail(const unsigned char* stage, con
   return true;
 }
 
-template <class T>
+template <class T, bool kBulk>
 __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(PhaseTables t) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* stage = smem;
@@ -848,8 +890,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
   }
 
   // ---- consumers (until the producer's end marker)
+  int held = -1;  // kBulk, warp 1: the stage its last bulk stores may still be reading
   for (int iter = 0;; ++iter)
-    if (!tma_consume_tail<T>(stage, meta, full, empty, iter, lane)) break;
+    if (!tma_consume_tail<T, kBulk>(stage, meta, full, empty, iter, lane, t.bulk_store, held)) break;
+  if (kBulk && (threadIdx.x >> 5) == 1) bulk_wait_all();  // stores complete before the CTA retires
 }
 
 // Single-GPU variant (items dealt round-robin, no scheduler state): the
@@ -1200,8 +1244,10 @@ struct PhaseK {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
         cudaFuncSetAttribute(box_phase_tma_static_kernel<T, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
-        cudaFuncSetAttribute(box_phase_tma_tail_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kTmaSmem));
+        cudaFuncSetAttribute(box_phase_tma_tail_kernel<T, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
+        cudaFuncSetAttribute(box_phase_tma_tail_kernel<T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
         return true;
       }();
       (void)configured;
@@ -1212,8 +1258,10 @@ struct PhaseK {
           box_phase_tma_static_kernel<T, true><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
         else
           box_phase_tma_static_kernel<T, false><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+      else if (t.bulk_store)
+        box_phase_tma_tail_kernel<T, true><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       else
-        box_phase_tma_tail_kernel<T><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+        box_phase_tma_tail_kernel<T, false><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
       return;
     }
     if (reduce)

@@ -322,7 +322,9 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_STREAM_SHARE(32), HS_PROG_STREAM_SHARE(51), HS_PROG_FUSE_PHASES,
                        HS_PROG_FANOUT_ONCE, HS_PROG_FANOUT_ONCE | HS_PROG_FUSE_PHASES,
                        HS_PROG_FANOUT_ONCE | HS_PROG_NO_SHARE,
-                       HS_PROG_PULL_MID | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL]
+                       HS_PROG_PULL_MID | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL,
+                       HS_PROG_NO_SHARE | HS_PROG_BULK_STORE,
+                       HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_BULK_STORE]
 AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE]
 TUNE_MARGIN = 0.01  # a later candidate must beat the best so far by 1% (timing noise)
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every

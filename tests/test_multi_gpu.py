@@ -34,7 +34,9 @@ def _gpus():
                                    # STATIC_LOCAL | PULL_MID | NO_STREAM, without / with BULK_STORE
                                    "16789504,50343936",
                                    # barriers as separate launches (default: folded into kernels)
-                                   "67108864,67121152"])
+                                   "67108864,67121152",
+                                   # TMA bulk stores (to peers when pushed): alone, NO_SHARE, fan-out once
+                                   "33554432,33554560,33587200"])
 def test_multi_gpu_parity(tmp_path, flags):
     n = int(os.environ.get("HS_TEST_RANKS", min(_gpus(), 8)))  # > GPUs: ranks share GPUs
     port = 29517 + sum(map(ord, flags)) % 300
