@@ -59,6 +59,7 @@ def main():
             dist.barrier()
             lay.fill_src(11, mode)
             lay.clear_dst()
+            ctx.barrier()  # hs_ctx_barrier: a device barrier between the runs as well
             ctx.sync()
             dist.barrier()
             prog.run()
