@@ -98,9 +98,6 @@ int main() {
       const float u = time_ms([&] { fan4_u4<<<148 * per_sm, 256>>>(s, d, d + m, d + 2 * m, d + 3 * m, m); });
       printf(", \"fan4_u4_%d_total\": %.0f", per_sm, 1.25 * bytes / (u * 1e-3) / 1e9);
     }
-    // 1:1 copy with the same code shape, for reference
-    const float c = time_ms([&] { fan4_u4<<<148 * 16, 256>>>(s, d, d, d, d, m); });
-    printf(", \"copy_u4_same_dst_total\": %.0f", 2.0 * bytes / 4 / (c * 1e-3) / 1e9);
   }
   printf("}\n");
   cudaError_t e = cudaDeviceSynchronize();
