@@ -220,12 +220,12 @@ def reference_arm(args, w, rank, world):
         probe = run_ref_tool(w, 512, 1, 0, threads)
         budget_s = 90.0
         steps = max(1, min(args.steps, int(budget_s / max(probe["seconds"], 1e-3))))
-        warm = min(args.warmup, 1)
+        warm = min(args.warmup, 5)  # each warm-up step is one bounded sample (~0.2 s)
         r = run_ref_tool(w, 512, steps, warm, threads)
         value = r["dst_bytes"] / r["seconds"] / 1e9
         cb = {"value": value, "unit": "GB/s", "cores": r["threads"], "kind": "reference",
               "sample": (f"{w.name} rows cut to {r['shape'][0]} per step, mean of {steps} timed "
-                         f"steps after {warm} warm-up (capped from --steps {args.steps} to fit "
+                         f"steps after {warm} warm-up steps (steps capped from {args.steps} to fit "
                          f"{budget_s:.0f} s); reference classify + reference Tensor primitives "
                          f"(oracle/ref_tool X), {r['threads']} threads")}
         ms = r["seconds"] * 1e3
