@@ -424,6 +424,59 @@ __device__ __forceinline__ void bulk_wait_read_but_last() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// HS_PROG_BULK_STORE, consumer side of a copy item (nterms == 1) in stage s.
+// The staged rows of the first min(nout, bulk_outs) outputs leave through TMA
+// bulk stores, one (output, row) per lane of consumer warp 1; all consumer
+// warps store the remaining outputs from registers, so fan-out copies keep
+// both store paths busy and the TMA unit is not monopolised by stores while it
+// must also feed the stages.  Warp 1 releases a stage one copy later, once
+// the stores have read it (`held`), so the store queue never drains between
+// items; outputs may be peer addresses.
+__device__ __forceinline__ void bulk_copy_item(const TmaRecHead* h, const TmaOperand* outs,
+                                               const unsigned char* in, int bulk_outs, uint64_t* empty,
+                                               int s, int& held) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, ctid = threadIdx.x - 32;
+  constexpr int nct = kTmaThreads - 32;
+  const int nvcol = h->nvcol, nvec = h->nrow * h->nvcol, no = h->nout;
+  const int nb = min(no, bulk_outs);
+  if (warp == 1) {
+    const int nrow = h->nrow;
+    const uint32_t row_bytes = static_cast<uint32_t>(nvcol) * 16;
+    for (int j = lane; j < nb * nrow; j += 32) {
+      const int o = j / nrow, r = j - o * nrow;
+      bulk_s2g(outs[o].row0 + r * outs[o].step, smem_u32(in) + r * row_bytes, row_bytes);
+    }
+    bulk_commit();
+  }
+  if (no > nb)
+    for (int v = ctid; v < nvec; v += nct) {
+      const int r = v / nvcol;
+      const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
+      const uint4 val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
+      for (int o = nb; o < no; ++o) __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
+    }
+  if (warp == 1) {
+    if (held >= 0) {
+      bulk_wait_read_but_last();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[held]);
+    }
+    held = s;
+  } else {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// Before a non-copy item: warp 1 releases the stage its bulk stores held.
+__device__ __forceinline__ void bulk_release_held(uint64_t* empty, int& held) {
+  if ((threadIdx.x >> 5) != 1 || held < 0) return;
+  bulk_wait_read_all();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[held]);
+  held = -1;
+}
+
 // Streamed launches, signalling side.  A system-scope fence in an SM that is
 // streaming costs microseconds (it waits for the SM's outstanding memory
 // traffic), so consumer warps never issue one: each consumer warp of an item
@@ -749,45 +802,11 @@ __device__ __forceinline__ bool tma_consume_tail(const unsigned char* stage, con
   const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;
   const unsigned char* in = stage + s * kStageBytes;
   if constexpr (kBulk) {
-    const int warp = threadIdx.x >> 5;
-    if (nt == 1) {  // as in box_phase_tma_static_kernel: outputs may be peer addresses
-      const int nb = min(no, bulk_outs);
-      if (warp == 1) {
-        const int nrow = h->nrow;
-        const uint32_t row_bytes = static_cast<uint32_t>(nvcol) * 16;
-        for (int j = lane; j < nb * nrow; j += 32) {
-          const int o = j / nrow, r = j - o * nrow;
-          bulk_s2g(outs[o].row0 + r * outs[o].step, smem_u32(in) + r * row_bytes, row_bytes);
-        }
-        bulk_commit();
-      }
-      if (no > nb)
-        for (int v = ctid; v < nvec; v += nct) {
-          const int r = v / nvcol;
-          const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
-          const uint4 val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
-          for (int o = nb; o < no; ++o)
-            __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
-        }
-      if (warp == 1) {
-        if (held >= 0) {
-          bulk_wait_read_but_last();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[held]);
-        }
-        held = s;
-      } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
+    if (nt == 1) {  // outputs may be peer addresses (pushed copies)
+      bulk_copy_item(h, outs, in, bulk_outs, empty, s, held);
       return true;
     }
-    if (warp == 1 && held >= 0) {  // a non-copy item: release the held stage first
-      bulk_wait_read_all();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[held]);
-      held = -1;
-    }
+    bulk_release_held(empty, held);
   }
   for (int v = ctid; v < nvec; v += nct) {
     const int r = v / nvcol;
@@ -973,50 +992,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     const TmaOperand* outs = reinterpret_cast<const TmaOperand*>(m + kTmaHeadWords) + nt;
     const unsigned char* in = stage + s * kStageBytes;
     if (kBulk && nt == 1) {
-      // A copy: the staged rows of the first nb outputs leave through TMA
-      // bulk stores, one (output, row) per lane of the first consumer warp;
-      // all consumer warps store the remaining outputs from registers, so
-      // fan-out copies keep both store paths busy and the TMA unit is not
-      // monopolised by stores while it must also feed the stages.  The first
-      // warp releases a stage one copy later, once the stores have read it,
-      // so the store queue never drains between items.
-      const int nb = min(no, t.bulk_store);
-      if (warp == 1) {
-        const int nrow = h->nrow;
-        const uint32_t row_bytes = static_cast<uint32_t>(nvcol) * 16;
-        for (int j = lane; j < nb * nrow; j += 32) {
-          const int o = j / nrow, r = j - o * nrow;
-          bulk_s2g(outs[o].row0 + r * outs[o].step, smem_u32(in) + r * row_bytes, row_bytes);
-        }
-        bulk_commit();
-      }
-      if (no > nb)
-        for (int v = ctid; v < nvec; v += nct) {
-          const int r = v / nvcol;
-          const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
-          const uint4 val = *reinterpret_cast<const uint4*>(in + static_cast<size_t>(v) * 16);
-          for (int o = nb; o < no; ++o)
-            __stcs(reinterpret_cast<uint4*>(outs[o].row0 + r * outs[o].step + cb), val);
-        }
-      if (warp == 1) {
-        if (held >= 0) {
-          bulk_wait_read_but_last();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[held]);
-        }
-        held = s;
-      } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
+      bulk_copy_item(h, outs, in, t.bulk_store, empty, s, held);
       continue;
     }
-    if (kBulk && warp == 1 && held >= 0) {  // a non-copy item: release the held stage first
-      bulk_wait_read_all();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[held]);
-      held = -1;
-    }
+    if (kBulk) bulk_release_held(empty, held);
     for (int v = ctid; v < nvec; v += nct) {
       const int r = v / nvcol;
       const int64_t cb = static_cast<int64_t>(v - r * nvcol) * 16;
