@@ -314,7 +314,7 @@ def main():
     tune_log = {}
 
     def prog_flags(prog, tuned):
-        return min(tuned, key=tuned.get) if tuned else args.flags
+        return prog.flags  # what autotune returned (its 1% margin can keep an earlier candidate)
 
     def timed(prog, steps, warmup, profile=False):
         for _ in range(warmup):

@@ -1386,7 +1386,10 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     // pipeline stage (nterms x item bytes <= kStageBytes).
     const int64_t row_vecs = static_cast<int64_t>(td.n[0]) * es_ / vb;
     int64_t item_bytes = kItemBytes;
-    if (tma) item_bytes = std::min<int64_t>(kTmaItemBytes, kStageBytes / std::max(1, td.nterms));
+    if (tma) {
+      const int64_t cap = (flags_ & HS_PROG_SMALL_ITEMS) ? kTmaItemBytes / 2 : kTmaItemBytes;
+      item_bytes = std::min<int64_t>(cap, kStageBytes / std::max(1, td.nterms));
+    }
     const int64_t target = std::max<int64_t>(1, item_bytes / vb);
     const int64_t planes = static_cast<int64_t>(td.n[2]) * td.n[3];
     std::vector<WorkItem>& items = H.items[slot_of(vb, tma, td.nterms >= 2)];

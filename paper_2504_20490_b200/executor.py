@@ -44,6 +44,7 @@ HS_PROG_FANOUT_ONCE = 32768  # world > 1: one NVLink store per remote GPU, local
 HS_PROG_STATIC_LOCAL = 1 << 24  # world > 1: static dealing for uniform local-only launches
 HS_PROG_BULK_STORE = 1 << 25  # static TMA kernel: copies' first two outputs leave through TMA bulk stores
 HS_PROG_SEPARATE_BARRIERS = 1 << 26  # world > 1: barriers as their own launches, not kernel prologues
+HS_PROG_SMALL_ITEMS = 1 << 27  # 16 KB TMA work items (plan-dependent; autotuned at N=1)
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -325,7 +326,7 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_PULL_MID | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL,
                        HS_PROG_NO_SHARE | HS_PROG_BULK_STORE,
                        HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_BULK_STORE]
-AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE]
+AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE, HS_PROG_SMALL_ITEMS, HS_PROG_SMALL_ITEMS | HS_PROG_BULK_STORE]
 TUNE_MARGIN = 0.01  # a later candidate must beat the best so far by 1% (timing noise)
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every
 # BASELINE plan at N=2, so it is not a default candidate.
@@ -337,8 +338,9 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
 
     Every candidate is compiled and timed for `steps` runs with CUDA events on `stream`; the
     max over ranks decides (all ranks take the same choice).  Results are bit-identical across
-    variants -- only the placement of work between ranks, or the store path, differs.  At
-    world == 1 the only variant is HS_PROG_BULK_STORE, for plans with copy tasks.
+    variants -- only the placement of work between ranks, the store path or the item size
+    differs.  At world == 1 the variants are HS_PROG_BULK_STORE and HS_PROG_SMALL_ITEMS, for
+    plans with copy tasks.
     Returns (program, {flags: ms}).
     """
     import torch

@@ -26,8 +26,9 @@ from paper_2504_20490_b200 import workloads as W
 pytestmark = pytest.mark.gpu
 
 
-# default (fused, TMA, merged outputs), the plain register path, TMA bulk stores for copies
-FLAG_SETS = [0, 2 | 4 | 8, 1 << 25]
+# default (fused, TMA, merged outputs), the plain register path, TMA bulk stores for
+# copies with 16 KB items
+FLAG_SETS = [0, 2 | 4 | 8, (1 << 25) | (1 << 27)]
 
 
 def _gpu_case(ctx, plan, src, dst, shape, dtype, seed, mode, n_virtual=10, flag_sets=FLAG_SETS):
