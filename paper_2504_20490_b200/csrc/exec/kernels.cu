@@ -1,14 +1,19 @@
 // hshard-b200 executor kernels (sm_100a).
 //
-// box_phase_tma_kernel (16-byte-aligned items, the hot path):
-//   one persistent CTA per SM, warp-specialised.  Lane 0 of warp 0 is the
-//   producer: for each work item it arms a stage's mbarrier with the item's
-//   byte count and issues one cp.async.bulk (TMA bulk copy, global ->
-//   shared) per (term, row) segment.  Warps 1..15 consume: wait for the stage,
-//   read every term from shared memory, form the grouped ordered sum in the
-//   dtype's accumulator, and store the result (st.global.cs) to every output.
-//   Four 48 KB stages keep up to ~144 KB per SM in flight independently of
-//   register pressure, which is what an HBM3e stream needs.
+// TMA pipeline (16-byte-aligned items, the hot path): one persistent CTA per
+//   SM, warp-specialised.  Warp 0 is the producer: for each work item it arms
+//   a stage's mbarrier with the item's byte count and its lanes issue one
+//   cp.async.bulk (TMA bulk copy, global -> shared) per (term, row) segment.
+//   16 consumer warps wait for the stage, read every term from shared memory,
+//   form the grouped ordered sum in the dtype's accumulator (packed f32x2 /
+//   bf16x2 where the dtype allows) and store the result (st.global.cs, or TMA
+//   bulk stores for copies under HS_PROG_BULK_STORE) to every output.  Four
+//   48 KB stages keep ~144 KB per SM in flight independently of register
+//   pressure, which is what an HBM3e stream needs.  Three schedulers:
+//     box_phase_tma_static_kernel  items dealt round-robin (N=1, uniform local launches)
+//     box_phase_tma_tail_kernel    15/16 static, the tail dynamic (unstreamed N>1)
+//     box_phase_tma_kernel         two dynamic queues, ready flags, signaller warp (streamed N>1)
+//   Each can open with the phase's cross-rank barrier (folded_barrier).
 // box_phase_kernel (any vector width): the register path, used for boxes
 //   whose pointers / strides / row lengths are not 16-byte aligned.
 #include <cstdint>
