@@ -227,6 +227,10 @@ int hs_ctx_sync(hs_ctx* ctx);
  * rank must call it; a rank that never arrives is reported as
  * DeadlockDetected by hs_ctx_sync.  No-op at world 1. */
 int hs_ctx_barrier(hs_ctx* ctx, void* stream);
+/* Clear a recorded DeadlockDetected (a timed-out barrier or ready-flag wait)
+ * once every rank has drained, so the context can run again.  Kernels that
+ * gave up still retire from their scheduler, so programs stay reusable. */
+int hs_ctx_clear_error(hs_ctx* ctx);
 
 #ifdef __cplusplus
 }

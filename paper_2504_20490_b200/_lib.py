@@ -89,6 +89,7 @@ def _load() -> ctypes.CDLL:
         "hs_ctx_write": (c_int, [c_void_p, c_size_t, c_void_p, c_size_t]),
         "hs_ctx_sync": (c_int, [c_void_p]),
         "hs_ctx_barrier": (c_int, [c_void_p, c_void_p]),
+        "hs_ctx_clear_error": (c_int, [c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name, None)

@@ -227,4 +227,8 @@ int hs_ctx_barrier(hs_ctx* ctx, void* stream) {
   return guarded([&] { ctx->c->barrier(stream ? static_cast<cudaStream_t>(stream) : ctx->c->stream()); });
 }
 
+int hs_ctx_clear_error(hs_ctx* ctx) {
+  return guarded([&] { ctx->c->clear_error(); });
+}
+
 }  // extern "C"

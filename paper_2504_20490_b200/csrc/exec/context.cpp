@@ -151,4 +151,10 @@ void Context::check_barrier_error() {
   if (err) fail(Errc::DeadlockDetected, "cross-rank barrier timed out (a peer never arrived)");
 }
 
+void Context::clear_error() {
+  if (analysis_) return;
+  cuda_check(cudaDeviceSynchronize(), "clear_error sync");
+  cuda_check(cudaMemset(barrier_error_, 0, sizeof(int)), "clear_error");
+}
+
 }  // namespace hshard::exec

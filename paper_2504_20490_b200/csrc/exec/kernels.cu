@@ -546,6 +546,16 @@ __device__ void tma_signaller(const PhaseTables& t, SigRing* ring, int lane) {
   }
 }
 
+// Dynamic-schedule kernels: a CTA leaving the launch counts itself out; the
+// last one resets the scheduler words for the program's next run.
+__device__ __forceinline__ void sched_retire(const PhaseTables& t) {
+  if (atomicAdd(&t.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+    t.sched[0] = 0;
+    t.sched[1] = 0;
+    t.sched[2] = 0;
+  }
+}
+
 // Streamed launches: the producer warp's lane 0 waits until a consumer
 // piece's producers have all signalled this run; bounded by ~10 s, after
 // which it records DeadlockDetected and proceeds (never a hang).
@@ -671,7 +681,10 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
     __syncthreads();
     const int good = *ok;
     __syncthreads();  // every thread has read it before the producer reuses meta
-    if (!good) return;
+    if (!good) {  // timed out (error recorded): still retire from the scheduler
+      if (threadIdx.x == 0) sched_retire(t);
+      return;
+    }
   }
   const int W = t.rec_words;
 
@@ -855,7 +868,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
     __syncthreads();
     const int good = *ok;
     __syncthreads();  // every thread has read it before the producer reuses meta
-    if (!good) return;
+    if (!good) {  // timed out (error recorded): still retire from the scheduler
+      if (threadIdx.x == 0) sched_retire(t);
+      return;
+    }
   }
   const int W = t.rec_words;
 

@@ -105,6 +105,15 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
       L.region = reg;
       L.rank = v_to_rank_[d];
       L.offset = offs ? offs[static_cast<size_t>(t) * n_virt_ + d] : SIZE_MAX;
+      // Every rank's arena has the same size: a caller-supplied offset must
+      // leave room for the whole shard (hs_fill_shard / hs_ctx_read check the same).
+      if (L.offset != SIZE_MAX) {
+        const size_t bytes = static_cast<size_t>(reg.cells()) * static_cast<size_t>(es_);
+        if (L.offset > ctx_.arena_bytes() || bytes > ctx_.arena_bytes() - L.offset)
+          fail(Errc::ShapeMismatch, "shard of device " + std::to_string(d) + " at offset " +
+                                        std::to_string(L.offset) + " (" + std::to_string(bytes) +
+                                        " bytes) exceeds the arena");
+      }
       L.subgroup = a.subgroup_of(d);
       L.eff_hdim = a.effective_hdim();
       states_[state][{t, d}] = L;
@@ -1721,6 +1730,11 @@ void Program::run_host_async(const void* const* src_host, void* const* dst_host,
   cuda_check(cudaStreamWaitEvent(compute, host_ev_[0], 0), "stream wait");
   cuda_check(cudaStreamWaitEvent(compute, host_ev_[2], 0), "stream wait");
   run(compute);
+  // host_ev_[1] (which the next call's H2D into these sources waits for) is
+  // recorded after every rank has finished this run: peers read this rank's
+  // sources over NVLink.  run() already ends with this barrier when its last
+  // launch stores into peers' destinations.
+  if (ctx_.world() > 1 && !nccl_mode_ && !remote_final_writes_) ctx_.barrier(compute);
   cuda_check(cudaEventRecord(host_ev_[1], compute), "event record");
   cuda_check(cudaStreamWaitEvent(d2h, host_ev_[1], 0), "stream wait");
   for (const auto& [d, t, off, bytes] : host_dst_) {
@@ -1737,6 +1751,10 @@ void Program::run_host(const void* const* src_host, void* const* dst_host) {
     if (h) cuda_check(cudaMemcpyAsync(ctx_.arena() + off, h, bytes, cudaMemcpyHostToDevice, s), "H2D");
   }
   run(s);
+  // Peers read this rank's sources over NVLink during their run: the next
+  // call's H2D (stream order: after this barrier) must not overwrite them
+  // before every rank has finished this run.
+  if (ctx_.world() > 1 && !nccl_mode_ && !remote_final_writes_) ctx_.barrier(s);
   for (const auto& [d, t, off, bytes] : host_dst_) {
     void* h = dst_host[static_cast<size_t>(t) * n_virt_ + d];
     if (h) cuda_check(cudaMemcpyAsync(h, ctx_.arena() + off, bytes, cudaMemcpyDeviceToHost, s), "D2H");

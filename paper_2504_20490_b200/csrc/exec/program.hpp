@@ -54,6 +54,9 @@ class Context {
   unsigned int next_epoch() { return ++epoch_; }
   unsigned int* const* peer_flag_table() const { return d_peer_flags_; }
   void check_barrier_error();
+  // Clears a recorded DeadlockDetected (after the caller has drained every
+  // rank), so the context can run again.
+  void clear_error();
 
   unsigned long long* scratch_counter() const { return counter_; }
   int* error_flag() const { return barrier_error_; }

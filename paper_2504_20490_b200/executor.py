@@ -131,6 +131,10 @@ class Context:
         """Device-side cross-rank barrier enqueued on `stream` (a cuda stream handle; None = ctx stream)."""
         check(LIB.hs_ctx_barrier(self._h, c_void_p(stream or 0)))
 
+    def clear_error(self) -> None:
+        """Clear a recorded DeadlockDetected once every rank has drained (hs_ctx_clear_error)."""
+        check(LIB.hs_ctx_clear_error(self._h))
+
     def close(self) -> None:
         h, self._h = getattr(self, "_h", None), None
         if h:
@@ -359,6 +363,15 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
         try:
             prog = Program(ctx, plan, layout, flags)
         except H.HshardError:  # a variant this plan cannot take (e.g. a box shape a rewrite does not support)
+            prog = None
+        if ctx.world > 1:
+            # compile checks only see this rank's tasks: every rank skips together
+            ok = torch.tensor([0.0 if prog is None else 1.0], dtype=torch.float64)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if ok.item() == 0.0 and prog is not None:
+                prog.close()
+                prog = None
+        if prog is None:
             continue
         two_phase_only = (HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_PULL_MID | HS_PROG_STREAM_SHARE(0xFF)
                           | HS_PROG_FUSE_PHASES | HS_PROG_CE_RELAY)
