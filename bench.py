@@ -17,10 +17,13 @@ e2e      = the same metric through the C-ABI host-buffer path
 roofline = the dominant kernel (the plan phase with the largest share of the
            step), algorithmic bytes per launch / its event-timed duration vs the
            measured HBM copy peak (N=1) or NVLink (N>1, per direction).
-cpu_baseline (rank 0, N=1) = the reference planner + the reference's own
-           per-cell Tensor primitives (oracle/_ref/ref_tool, command X) on a
-           bounded row-sample of the same workload, all host threads.
---impl reference = that CPU path alone, as the reference arm.
+cpu_baseline (rank 0, N=1) = the reference planner + the CPU memcpy executor
+           (oracle/_ref/ref_tool N: native dtype, row memcpy, fp32 sums) on the
+           full workload, all host threads; cpu_baselines adds it at 1 thread
+           and the reference's own per-cell Tensor primitives (command X) on a
+           row sample.
+--impl reference = the reference's own CPU path (ref_tool X) on the FULL
+           workload, all host threads, without loading any product code.
 """
 from __future__ import annotations
 
@@ -145,98 +148,124 @@ def ncu_traffic(workload: str, phase: int):
 
 
 # ---------------------------------------------------------------- cpu / reference
-def sample_transition(w, rows_cap: int):
-    """Bounded sample of a classify workload: the first dim cut to rows_cap."""
-    tid, src, dst, shape = w.transitions[0]
-    shape = list(shape)
-    if shape[0] > rows_cap:
-        shape[0] = rows_cap
-    return src, dst, shape
+# Element widths of the workload dtypes, kept local so the reference arm never
+# imports the product bindings (no libhshard_b200.so in that process).
+DTYPE_BYTES = {"f32": 4, "f64": 8, "i32": 4, "i64": 8, "bf16": 2}
 
 
-def run_ref_tool(w, rows_cap: int, reps: int, warmup: int, threads: int):
-    src, dst, shape = sample_transition(w, rows_cap)
-    dt = "f32" if w.dtype == "bf16" else w.dtype  # reference DType has no bf16
-    cmd = f"X|{dt}|{','.join(map(str, shape))}|u|{src}|{dst}|1|grid|{reps}|0|{threads}|{warmup}\n"
-    out = subprocess.run([REF_TOOL], input=cmd, capture_output=True, text=True, timeout=3600)
-    j = json.loads(out.stdout.strip().splitlines()[-1])
+def _ref_tool(cmd: str, timeout: float = 3600.0) -> dict:
+    out = subprocess.run([REF_TOOL], input=cmd, capture_output=True, text=True, timeout=timeout)
+    lines = out.stdout.strip().splitlines()
+    j = json.loads(lines[-1]) if lines else {"error": "no output", "stderr": out.stderr[-300:]}
     if "error" in j:
         raise RuntimeError(j)
-    from paper_2504_20490_b200 import hshard as H
-    # dst-resident bytes of the sample in the workload's dtype
-    es = H.DTYPE_BYTES[w.dtype]
-    dst_bytes = j["dst_bytes"] // H.DTYPE_BYTES[dt] * es
+    return j
+
+
+def _shape_rows(shape, rows_cap):
+    shape = list(shape)
+    if rows_cap and shape[0] > rows_cap:
+        shape[0] = rows_cap
+    return shape
+
+
+def reference_primitive_run(w, reps: int, warmup: int, threads: int, rows_cap=None) -> dict:
+    """oracle/_ref/ref_tool X: the reference planner's classify + the reference's own per-cell
+    Tensor::slice / write_slice / add_slice (tensor.cpp:84-114) driven per SPEC.md:467-495,
+    row bands of every target spread over `threads` host threads.  The reference Tensor stores
+    doubles for every dtype (tensor.hpp:24-30) and its DType has no BF16 (common.hpp:28), so a
+    bf16 workload is planned as F32 (identical plan) and its bytes are counted in bf16."""
+    tid, src, dst, shape = w.transitions[0]
+    shape = _shape_rows(shape, rows_cap)
+    dt = "f32" if w.dtype == "bf16" else w.dtype
+    j = _ref_tool(f"X|{dt}|{','.join(map(str, shape))}|u|{src}|{dst}|1|grid|{reps}|0|{threads}|{warmup}\n")
+    dst_bytes = j["dst_bytes"] // DTYPE_BYTES[dt] * DTYPE_BYTES[w.dtype]
     return {"seconds": j["mean"], "best": j["seconds"], "dst_bytes": dst_bytes, "shape": shape,
-            "threads": j["threads"]}
+            "threads": j["threads"], "reps": j["reps"]}
 
 
-def cpu_baseline(w, rows_cap=1024, reps=3, warmup=1):
-    threads = os.cpu_count() or 1
-    if os.path.exists(REF_TOOL) and w.kind == "classify":
-        r = run_ref_tool(w, rows_cap, reps, warmup, threads)
-        return {"value": r["dst_bytes"] / r["seconds"] / 1e9, "unit": "GB/s", "cores": r["threads"],
-                "kind": "reference",
-                "sample": (f"{w.name} rows cut to {r['shape'][0]} (shape {r['shape']}), mean of "
-                           f"{reps} runs after {warmup} warm-up; reference classify + reference "
-                           "Tensor::slice/write_slice/add_slice (tensor.cpp:84-114) driven per "
-                           "SPEC.md:467-495 by oracle/ref_tool.cpp, split by target device over "
-                           f"{r['threads']} threads; doubles per cell (tensor.hpp:24)")}
-    # numpy oracle port (switch workloads, or no reference build)
-    import numpy as np
-    from oracle import executor as ox
-    from paper_2504_20490_b200 import hshard as H
-    if w.kind == "classify":
-        src, dst, shape = sample_transition(w, rows_cap)
-        plan = H.classify(src, dst, shape, w.dtype).json()
-        shards = ox.scatter(src, shape, w.dtype, 1)
-        t0 = time.perf_counter()
-        out = ox.execute_plan(plan, shards, w.dtype)
-        sec = time.perf_counter() - t0
-        nbytes = sum(a.nbytes for a in out.values())
-        sample = f"{w.name} rows cut to {shape[0]}, numpy oracle port (oracle/executor.py)"
-    else:
-        entries = [e for e in w.transitions if len(e[3]) == 2][:12]
-        plan = H.plan_switch(entries, w.dtype).json()
-        src = {}
-        for tid, s, d, shp in entries:
-            for dev, a in ox.scatter(s, shp, w.dtype, 1, tid).items():
-                src[(tid, dev)] = a
-        t0 = time.perf_counter()
-        out = ox.execute_switch(plan, entries, src, w.dtype)
-        sec = time.perf_counter() - t0
-        nbytes = sum(a.nbytes for a in out.values())
-        sample = f"{w.name}: first {len(entries)} 2-d parameters, numpy oracle port"
-    return {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": sample}
+def native_run(w, reps: int, warmup: int, threads: int) -> dict:
+    """oracle/_ref/ref_tool N: the reference planner's plan on the CPU memcpy executor
+    (oracle/native_exec.inc): native-dtype shards, one memcpy per
+    contiguous row, fp32 accumulation in ascending device-id order, host threads over rows."""
+    tid, src, dst, shape = w.transitions[0]
+    j = _ref_tool(f"N|{w.dtype}|{','.join(map(str, shape))}|u|{src}|{dst}|1|grid|{reps}|{threads}|{warmup}|-\n")
+    return j
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baselines(w):
+    """Rank 0, N=1: the CPU executors on the box's host cores, same workload.
+    [0] native memcpy executor, all host threads (the line's cpu_baseline);
+    [1] the same at 1 thread; [2] the reference's own Tensor primitives on a
+    row sample (the full-size run is the --impl reference arm)."""
+    if not os.path.exists(REF_TOOL) or w.kind != "classify":
+        return [{"value": None, "unit": "GB/s", "cores": 0, "kind": "port",
+                 "sample": "unavailable: oracle/_ref/ref_tool missing or not a single-tensor workload"}]
+    nproc = os.cpu_count() or 1
+    model = cpu_model()
+    out = []
+    for threads, reps in ((nproc, 10), (1, 3)):
+        j = native_run(w, reps, 1, threads)
+        out.append({"value": j["dst_bytes"] / j["mean"] / 1e9, "unit": "GB/s", "cores": j["threads"],
+                    "kind": "port", "ms_per_step": j["mean"] * 1e3, "cpu_model": j.get("cpu_model", model),
+                    "nproc": nproc,
+                    "sample": (f"{w.name} at full size {list(w.transitions[0][3])}, mean of {reps} runs after "
+                               f"1 warm-up; reference planner (classify) + CPU memcpy executor "
+                               f"(oracle/native_exec.inc: native {w.dtype} shards, row memcpy, fp32 "
+                               f"ascending-id sums; outputs preallocated like the GPU path's) on "
+                               f"{j['threads']} host thread(s)")})
+    r = reference_primitive_run(w, 2, 1, nproc, rows_cap=1024)
+    out.append({"value": r["dst_bytes"] / r["seconds"] / 1e9, "unit": "GB/s", "cores": r["threads"],
+                "kind": "reference", "ms_per_step": r["seconds"] * 1e3, "cpu_model": model, "nproc": nproc,
+                "sample": (f"{w.name} rows cut to {r['shape'][0]} (shape {r['shape']}), mean of 2 runs "
+                           "after 1 warm-up; reference classify + reference Tensor::slice/write_slice/"
+                           "add_slice (tensor.cpp:84-114), doubles per cell, row bands over "
+                           f"{r['threads']} threads (oracle/_ref/ref_tool X)")})
+    return out
 
 
 def reference_arm(args, w, rank, world):
+    """--impl reference: the reference's own CPU path (oracle/_ref/ref_tool X) on the FULL
+    workload, all host threads, rank 0 only.  No product code is imported or loaded."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    if os.path.exists(REF_TOOL) and w.kind == "classify":
-        # Each step is a bounded row-sample of the workload; the number of
-        # timed steps is capped so the whole arm stays within ~2 minutes.
-        probe = run_ref_tool(w, 512, 1, 0, threads)
-        budget_s = 90.0
-        steps = max(1, min(args.steps, int(budget_s / max(probe["seconds"], 1e-3))))
-        warm = min(args.warmup, 5)  # each warm-up step is one bounded sample (~0.2 s)
-        r = run_ref_tool(w, 512, steps, warm, threads)
-        value = r["dst_bytes"] / r["seconds"] / 1e9
-        cb = {"value": value, "unit": "GB/s", "cores": r["threads"], "kind": "reference",
-              "sample": (f"{w.name} rows cut to {r['shape'][0]} per step, mean of {steps} timed "
-                         f"steps after {warm} warm-up steps (steps capped from {args.steps} to fit "
-                         f"{budget_s:.0f} s); reference classify + reference Tensor primitives "
-                         f"(oracle/ref_tool X), {r['threads']} threads")}
-        ms = r["seconds"] * 1e3
-    else:
-        cb = cpu_baseline(w)
-        value, ms = cb["value"], None
+    if not (os.path.exists(REF_TOOL) and w.kind == "classify"):
+        print(json.dumps({"impl": "reference", "unavailable": f"no CPU reference for {w.name} "
+                          "(oracle/_ref/ref_tool missing or a switch workload)"}), flush=True)
+        return
+    # one timed probe step sizes the run: the whole arm stays within ~4 minutes
+    probe = reference_primitive_run(w, 1, 0, threads)
+    budget_s = 240.0
+    steps = max(1, min(args.steps, int(budget_s / max(probe["seconds"], 1e-3))))
+    warm = min(args.warmup, 1)
+    r = reference_primitive_run(w, steps, warm, threads)
+    value = r["dst_bytes"] / r["seconds"] / 1e9
+    sample = (f"{w.name} at full size {r['shape']}: mean of {r['reps']} timed steps after {warm} warm-up "
+              f"step(s){'' if steps == args.steps else f' (capped from {args.steps} to fit {budget_s:.0f} s)'}; "
+              "reference classify + reference Tensor::slice/write_slice/add_slice (tensor.cpp:84-114) "
+              "driven per SPEC.md:467-495 (oracle/_ref/ref_tool X), row bands of every target over "
+              f"{r['threads']} host threads; the reference Tensor stores doubles for every dtype "
+              f"(tensor.hpp:24-30), bytes counted in {w.dtype}")
+    cb = {"value": value, "unit": "GB/s", "cores": r["threads"], "kind": "reference", "sample": sample,
+          "cpu_model": cpu_model()}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
             "data": "synthetic (counter-hash grid payload)",
-            "config": {"workload": w.name, "sample": cb["sample"]},
+            "config": {"workload": w.name, "shape": r["shape"], "n_virtual": w.n_virtual,
+                       "dst_resident_bytes": r["dst_bytes"], "same_config": True},
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -249,15 +278,13 @@ def main():
     from paper_2504_20490_b200 import workloads as W
     w = W.by_name(args.config)
 
+    if args.impl == "reference":
+        # rank 0 alone, no process group, no torch, no product library
+        reference_arm(args, w, rank, world)
+        return
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group(backend="cpu:gloo,cuda:nccl")
-    if args.impl == "reference":
-        reference_arm(args, w, rank, world)
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
-        return
 
     import numpy as np
     import torch
@@ -549,12 +576,13 @@ def main():
             del sprog, slay
             ctx.reset(0)
 
-    cb = None
+    cb, cbs = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cb = cpu_baseline(w)
+            cbs = cpu_baselines(w)
+            cb = cbs[0]
         except Exception as e:  # reported, never fatal for the GPU number
-            cb = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+            cb = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
                   "sample": f"failed: {e}"}
 
     if rank == 0:
@@ -571,7 +599,8 @@ def main():
                        "program": {k: st[k] for k in ("phases", "plan_phases", "tasks", "items",
                                                       "fused_tasks", "tma_items", "hbm_read",
                                                       "hbm_write", "nvlink_in", "nvlink_out")}},
-            "roofline": roof, "floor": floor, "bus": busd, "cpu_baseline": cb, "e2e": e2e,
+            "roofline": roof, "floor": floor, "bus": busd, "cpu_baseline": cb, "cpu_baselines": cbs,
+            "e2e": e2e,
             "gpu_launches": args.steps * st["kernels_per_run"],
             "kernels_per_step": st["kernels_per_run"], "phase_ms": phase_ms,
             "verified": verified, "clocks": clk, "graph_switch": switch,

@@ -27,6 +27,11 @@
 //   V|shape|anno                              validate (issue codes)
 //   X|dtype|shape|bw|src|dst|seed|mode|reps|emit[|threads[|warmup]]
 //                                             reference-primitive executor
+//   N|dtype|shape|bw|src|dst|seed|mode|reps|threads|warmup|outdir
+//                                             native-dtype memcpy executor
+//   W|dtype|bw|n|seed|reps|threads|warmup + n lines tid|shape|src|dst
+//                                             the same for a fused switch
+//                                             (oracle/native_exec.inc)
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -34,6 +39,7 @@
 #include <cstdio>
 #include <cstring>
 #include <iostream>
+#include <optional>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -349,11 +355,29 @@ ShardMap init_target(const HetAnnotation& a, const Shape& shape, DType dt) {
 // Phase semantics per SURVEY Appendix C (restating SPEC.md:467-495) using the
 // reference's Tensor::slice / write_slice / add_slice.  Reductions use
 // ascending device id order; values are doubles (tensor.hpp:24).
-// Work is split by TARGET device across `nthreads` host threads (thread `tid`
-// owns targets d with d % nthreads == tid); targets are independent tensors.
+// Work units are (target device d, row band k of K): band k is rows
+// [lo + n*k/K, lo + n*(k+1)/K) of dim 0 of d's target box, and every logical
+// region written to d is clipped to it, so units write disjoint cells and the
+// primitives run unchanged on all host threads (unit u = d*K + k runs on
+// thread u % nthreads).  Whole-shard assignments (Identity / SendRecv) are
+// band 0's.
+struct Unit {
+  int tid = 0, nthreads = 1, K = 1;
+};
+
+std::optional<SliceRegion> clip(const SliceRegion& logical, const SliceRegion& target, int k, int K) {
+  if (K == 1) return logical;
+  SliceRegion band;
+  band.bounds = target.bounds;
+  const int64_t lo = target.bounds[0][0], n = target.bounds[0][1] - lo;
+  band.bounds[0] = {lo + n * k / K, lo + n * (k + 1) / K};
+  if (band.bounds[0][0] >= band.bounds[0][1]) return std::nullopt;
+  return intersect(logical, band);
+}
+
 void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardMap& in,
-              ShardMap& out, int tid = 0, int nthreads = 1) {
-  auto owns = [&](DeviceId d) { return d % nthreads == tid; };
+              ShardMap& out, const Unit& U) {
+  auto mine = [&](DeviceId d, int k) { return (static_cast<int64_t>(d) * U.K + k) % U.nthreads == U.tid; };
   auto piece = [&](DeviceId m, const SliceRegion& logical) {
     const auto& [reg, ten] = in.at(m);
     return ten.slice(local_box(reg, logical));
@@ -368,11 +392,11 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
   switch (step.kind) {
     case StepKind::Identity:
       for (DeviceId d : phase_src.dg_union.at(step.subgroup).devices)
-        if (owns(d)) out.at(d).second = in.at(d).second;
+        if (mine(d, 0)) out.at(d).second = in.at(d).second;
       break;
     case StepKind::SendRecv:
       for (auto [s, r] : step.pairs)
-        if (owns(r)) out.at(r).second = in.at(s).second;
+        if (mine(r, 0)) out.at(r).second = in.at(s).second;
       break;
     case StepKind::AllReduce:
     case StepKind::ReduceScatter:
@@ -380,17 +404,21 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
         std::vector<DeviceId> order(grp.begin(), grp.end());
         std::sort(order.begin(), order.end());
         for (DeviceId d : grp) {
-          if (!owns(d)) continue;
           SliceRegion target = out.at(d).first;
-          SliceRegion box;
-          box.bounds = target.bounds;
+          SliceRegion whole;
+          whole.bounds = target.bounds;
           for (DeviceId m : order) {
-            if (!in.at(m).first.covers(box)) throw Error(Errc::ShapeMismatch, "unexecutable");
+            if (!in.at(m).first.covers(whole)) throw Error(Errc::ShapeMismatch, "unexecutable");
           }
-          bool first = true;
-          for (DeviceId m : order) {
-            put(d, box, piece(m, box), !first);
-            first = false;
+          for (int k = 0; k < U.K; ++k) {
+            if (!mine(d, k)) continue;
+            auto box = clip(whole, target, k, U.K);
+            if (!box) continue;
+            bool first = true;
+            for (DeviceId m : order) {
+              put(d, *box, piece(m, *box), !first);
+              first = false;
+            }
           }
         }
       }
@@ -398,16 +426,22 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
     case StepKind::AllGather:
       for (const auto& grp : step.groups) {
         for (DeviceId d : grp) {
-          if (!owns(d)) continue;
           SliceRegion target = out.at(d).first;
           int64_t covered = 0;
           for (DeviceId m : grp) {
             auto isect = intersect(in.at(m).first, target);
-            if (!isect) continue;
-            covered += isect->cells();
-            put(d, *isect, piece(m, *isect), false);
+            if (isect) covered += isect->cells();
           }
           if (covered != target.cells()) throw Error(Errc::ShapeMismatch, "unexecutable");
+          for (int k = 0; k < U.K; ++k) {
+            if (!mine(d, k)) continue;
+            for (DeviceId m : grp) {
+              auto isect = intersect(in.at(m).first, target);
+              if (!isect) continue;
+              auto box = clip(*isect, target, k, U.K);
+              if (box) put(d, *box, piece(m, *box), false);
+            }
+          }
         }
       }
       break;
@@ -416,40 +450,53 @@ void run_step(const CommStep& step, const HetAnnotation& phase_src, const ShardM
     case StepKind::SplitAllGather:
       for (const auto& sc : step.slices) {
         for (DeviceId r : sc.receivers) {
-          if (!owns(r)) continue;
           const SliceRegion& rr = out.at(r).first;
           std::vector<DeviceId> cs(sc.contributors.begin(), sc.contributors.end());
           std::sort(cs.begin(), cs.end());
-          bool any = false;
-          for (DeviceId c : cs) {
-            const SliceRegion& cr = in.at(c).first;
-            if (cr.partial_index % rr.partial_count != rr.partial_index) continue;
-            put(r, sc.region, piece(c, sc.region), any);
-            any = true;
-          }
-          if (!any) {
-            Tensor z(sc.region.extents(), out.at(r).second.dtype);
-            put(r, sc.region, z, false);
+          for (int k = 0; k < U.K; ++k) {
+            if (!mine(r, k)) continue;
+            auto box = clip(sc.region, rr, k, U.K);
+            if (!box) continue;
+            bool any = false;
+            for (DeviceId c : cs) {
+              const SliceRegion& cr = in.at(c).first;
+              if (cr.partial_index % rr.partial_count != rr.partial_index) continue;
+              put(r, *box, piece(c, *box), any);
+              any = true;
+            }
+            if (!any) {
+              Tensor z(box->extents(), out.at(r).second.dtype);
+              put(r, *box, z, false);
+            }
           }
         }
       }
       break;
     case StepKind::Bsr:
-      for (const auto& c : step.bsr->local_copies)
-        if (owns(c.device)) put(c.device, c.region, piece(c.device, c.region), false);
-      for (const auto& fg : step.bsr->fusion_groups)
-        for (int i : fg.transfer_indices) {
-          const auto& t = step.bsr->transfers[i];
-          if (owns(t.receiver)) put(t.receiver, t.region, piece(t.sender, t.region), false);
+      for (int k = 0; k < U.K; ++k) {
+        for (const auto& c : step.bsr->local_copies) {
+          if (!mine(c.device, k)) continue;
+          auto box = clip(c.region, out.at(c.device).first, k, U.K);
+          if (box) put(c.device, *box, piece(c.device, *box), false);
         }
+        for (const auto& fg : step.bsr->fusion_groups)
+          for (int i : fg.transfer_indices) {
+            const auto& t = step.bsr->transfers[i];
+            if (!mine(t.receiver, k)) continue;
+            auto box = clip(t.region, out.at(t.receiver).first, k, U.K);
+            if (box) put(t.receiver, *box, piece(t.sender, *box), false);
+          }
+      }
       break;
   }
 }
 
 void run_phase(const std::vector<CommStep>& steps, const HetAnnotation& phase_src,
                const ShardMap& in, ShardMap& out, int nthreads) {
+  // K bands per target so that targets x bands covers every thread
+  const int K = std::max<int>(1, (nthreads + static_cast<int>(out.size()) - 1) / std::max<int>(1, out.size()));
   if (nthreads <= 1) {
-    for (const auto& s : steps) run_step(s, phase_src, in, out);
+    for (const auto& s : steps) run_step(s, phase_src, in, out, Unit{});
     return;
   }
   std::vector<std::thread> pool;
@@ -457,7 +504,7 @@ void run_phase(const std::vector<CommStep>& steps, const HetAnnotation& phase_sr
   for (int t = 0; t < nthreads; ++t)
     pool.emplace_back([&, t] {
       try {
-        for (const auto& s : steps) run_step(s, phase_src, in, out, t, nthreads);
+        for (const auto& s : steps) run_step(s, phase_src, in, out, Unit{t, nthreads, K});
       } catch (...) {
         errs[t] = std::current_exception();
       }
@@ -467,20 +514,21 @@ void run_phase(const std::vector<CommStep>& steps, const HetAnnotation& phase_sr
     if (e) std::rethrow_exception(e);
 }
 
+// The functional executor (sim.hpp:77-79): fresh target states per run; the
+// source map is read in place (no per-run copy of the inputs).
 ShardMap run_plan(const CommPlan& plan, const ShardMap& src, DType dt, int nthreads) {
   if (plan.bottom_phase.empty() && plan.top_phase.empty()) return src;
-  ShardMap cur = src;
+  const ShardMap* cur = &src;
+  ShardMap mid;
   if (!plan.bottom_phase.empty()) {
-    ShardMap next = init_target(plan.bottom_target(), plan.shape, dt);
-    run_phase(plan.bottom_phase, plan.src, cur, next, nthreads);
-    cur = std::move(next);
+    mid = init_target(plan.bottom_target(), plan.shape, dt);
+    run_phase(plan.bottom_phase, plan.src, *cur, mid, nthreads);
+    if (plan.top_phase.empty()) return mid;
+    cur = &mid;
   }
-  if (!plan.top_phase.empty()) {
-    ShardMap next = init_target(plan.dst, plan.shape, dt);
-    run_phase(plan.top_phase, plan.mid ? *plan.mid : plan.src, cur, next, nthreads);
-    cur = std::move(next);
-  }
-  return cur;
+  ShardMap next = init_target(plan.dst, plan.shape, dt);
+  run_phase(plan.top_phase, plan.mid ? *plan.mid : plan.src, *cur, next, nthreads);
+  return next;
 }
 
 std::string cmd_execute(const std::vector<std::string>& f) {
@@ -495,8 +543,14 @@ std::string cmd_execute(const std::vector<std::string>& f) {
   int warmup = f.size() > 11 ? std::stoi(f.at(11)) : 0;
   CommPlan plan = classify(src, dst, shape, dt, bw);
   ShardMap in;
-  for (DeviceId d : src.all_devices())
-    in.emplace(d, std::make_pair(placement(src, shape, d), make_shard(src, shape, d, seed, 0, dt)));
+  for (DeviceId d : src.all_devices())  // regions first, payloads generated in parallel below
+    in.emplace(d, std::make_pair(placement(src, shape, d), Tensor(Shape{}, dt)));
+  {
+    std::vector<std::thread> gen;
+    for (DeviceId d : src.all_devices())
+      gen.emplace_back([&, d] { in.at(d).second = make_shard(src, shape, d, seed, 0, dt); });
+    for (auto& th : gen) th.join();
+  }
   ShardMap out;
   for (int r = 0; r < warmup; ++r) out = run_plan(plan, in, dt, nthreads);
   double best = 1e30, total = 0;
@@ -537,6 +591,8 @@ std::string cmd_execute(const std::vector<std::string>& f) {
   o += "},\"dst_bytes\":" + std::to_string(dst_bytes) + "}";
   return o;
 }
+
+#include "native_exec.inc"
 
 // G|stmt&stmt&...: build the reference CompGraph from the line form of
 // include/hshard/graph.hpp (parse_graph), deduce every strategy with the
@@ -720,6 +776,8 @@ std::string handle(const std::string& line, std::istream& in) {
     return o + "]";
   }
   if (c == "X") return cmd_execute(f);
+  if (c == "N") return cmd_native(f);
+  if (c == "W") return cmd_native_switch(f, in);
   if (c == "G") return cmd_graph(line.substr(2));
   if (c == "S") return cmd_specialize(f, line);
   return "{\"error\":\"UnknownCommand\"}";

@@ -11,7 +11,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Dict, List, Sequence, Tuple
 
-from .hshard import anno, single
+from .annotext import anno, single
 
 Transition = Tuple[int, str, str, Tuple[int, ...]]
 

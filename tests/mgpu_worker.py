@@ -13,6 +13,7 @@ import traceback
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def main():
@@ -31,7 +32,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     dist.init_process_group("gloo")
     torch.cuda.set_device(local)
-    ctx = Context(8 << 30, rank=rank, world=world, gpu=local)
+    full = os.environ.get("HS_MGPU_FULL") == "1"
+    ctx = Context((40 if full else 8) << 30, rank=rank, world=world, gpu=local)
     flag_sets = [int(x) for x in os.environ.get("HS_MGPU_FLAGS", "0,14,1").split(",")]
     if any(f & 2048 for f in flag_sets):
         ctx.init_nccl()
@@ -41,6 +43,7 @@ def main():
         nonlocal ok
         mark = ctx.alloc(0)
         lay = ShardLayout(ctx, plan, n_virtual)
+        lay_holder[:] = [lay]
         for flags in flag_sets:
             # run 1 on other values, run 2 (flag epoch 2) on the checked ones:
             # a consumer that does not wait for this run's producers reads
@@ -79,7 +82,90 @@ def main():
             dist.barrier()
         ctx.reset(mark)
 
+    def full_size_cases():
+        """BASELINE reduction configs at FULL size with real-valued payloads; rank 0 runs
+        the native CPU executor (oracle/_ref/ref_tool N) into a shared directory and
+        every rank byte-compares its own destination shards with it."""
+        import tempfile
+
+        import native_ref
+        shared = os.environ["HS_MGPU_OUT"] + ".native"
+        for wname in os.environ.get("HS_MGPU_FULL_CASES", "cfg2e,cfg3b,cfg2a").split(","):
+            w = W.by_name(wname)
+            _, src, dst, shape = w.transitions[0]
+            plan = H.classify(src, dst, shape, w.dtype)
+            d = f"{shared}.{wname}"
+            if rank == 0:
+                os.makedirs(d, exist_ok=True)
+                native_ref.run(src, dst, shape, w.dtype, 11, "real", 0, d)
+            dist.barrier()
+
+            def src_of(d=d, w=w):
+                out = {}
+                for (slot, dev), rec in lay_holder[0].local("dst").items():
+                    out[(slot, dev)] = np.fromfile(os.path.join(d, f"dev{dev}.bin"),
+                                                   dtype=native_ref.NP[w.dtype]).reshape(rec["ext"])
+                return out
+            lay_holder.clear()
+            run_case(f"{wname}-full", plan, w.n_virtual, src_of, w.dtype, "real")
+
+    def host_path_case():
+        """hs_prog_run_host / run_host_async with DIFFERENT inputs every step and no
+        host-side barrier between steps: peers read this rank's sources over NVLink,
+        so a step's H2D must not overwrite them before every rank has finished the
+        previous run (program.cpp run_host)."""
+        w = W.by_name("cfg2e")
+        _, src, dst, _ = w.transitions[0]
+        shape = (256, 1024)
+        plan = H.classify(src, dst, shape, w.dtype)
+        seeds = [21, 22, 23, 24, 25]
+        srcs = {s_: ox.scatter(src, shape, w.dtype, s_, 0, "real") for s_ in seeds}
+        wants = {s_: ox.execute_plan(plan.json(), srcs[s_], w.dtype) for s_ in seeds}
+        bad = []
+        mark = ctx.alloc(0)
+        lays = [ShardLayout(ctx, plan, w.n_virtual) for _ in range(2)]
+        progs = [Program(ctx, plan, lay) for lay in lays]
+        local_src = {k: v for k, v in lays[0].local("src").items()}
+        dst_bufs = [{k: np.empty(rec["ext"], dtype=np.uint16) for k, rec in lay.local("dst").items()}
+                    for lay in lays]
+        host_src = {s_: {k: np.ascontiguousarray(srcs[s_][k[1]]) for k in local_src} for s_ in seeds}
+        dist.barrier()
+        for s_ in seeds:  # synchronous path, back to back
+            progs[0].run_host(host_src[s_], dst_bufs[0])
+            for k, a in dst_bufs[0].items():
+                if not np.array_equal(a, wants[s_][k[1]]):
+                    bad.append(("sync", s_, k[1]))
+        ctx.sync()
+        dist.barrier()
+        h2d, comp, d2h = (torch.cuda.Stream(device=local) for _ in range(3))
+        for i, s_ in enumerate(seeds):  # pipelined: two programs, inputs change every step
+            progs[i % 2].run_host_async(host_src[s_], dst_bufs[i % 2], h2d.cuda_stream, comp.cuda_stream,
+                                        d2h.cuda_stream)
+            if i >= 1:  # the previous step's outputs: complete once d2h has drained them
+                d2h.synchronize()
+                prev = seeds[i - 1]
+                for k, a in dst_bufs[(i - 1) % 2].items():
+                    if not np.array_equal(a, wants[prev][k[1]]):
+                        bad.append(("async", prev, k[1]))
+        d2h.synchronize()
+        for k, a in dst_bufs[(len(seeds) - 1) % 2].items():
+            if not np.array_equal(a, wants[seeds[-1]][k[1]]):
+                bad.append(("async", seeds[-1], k[1]))
+        ctx.sync()
+        for p_ in progs:
+            p_.close()
+        dist.barrier()
+        ctx.reset(mark)
+        results.append({"case": "host-path", "flags": 0, "bad": bad, "nvlink_in": 0, "nvlink_out": 0})
+        return not bad
+
+    lay_holder = []
     try:
+        if full:
+            full_size_cases()
+            raise StopIteration
+        if not host_path_case():
+            ok = False
         for wname, shape in [("cfg1A", (256, 64)), ("cfg1B", (256, 64)), ("cfg1D", (256, 64)),
                              ("cfg2e", (64, 256)), ("cfg2b", (64, 256)), ("cfg3b", (64, 512)),
                              ("cfg3a", (64, 512)), ("cfg3c", (60, 35))]:
@@ -113,6 +199,8 @@ def main():
             slot = {tid: i for i, (tid, _, _, _) in enumerate(entries)}
             return {(slot[tid], dev): a for (tid, dev), a in out.items()}
         run_case("switch-mini", plan, 8, sw_src, "bf16", "real")
+    except StopIteration:
+        pass
     except Exception:
         ok = False
         results.append({"error": traceback.format_exc()})

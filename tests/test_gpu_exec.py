@@ -7,9 +7,11 @@
   zero ulp against the oracle; against the reference's double-precision
   executor it is exact on the grid, see test_oracle.py);
 * the on-GPU payload generator must equal oracle/datagen.py;
-* BASELINE workloads at FULL size: configs 1-2 against the oracle, configs
-  3-5 through size-independent properties (every Partial-free destination
-  shard equals the logical counter-hash tensor on its box);
+* BASELINE workloads at FULL size: configs 1-2 against the oracle; every
+  reduction config (2a/2b/2d/2e, 3a/3b/3c) with real-valued, order-sensitive
+  payloads against the native CPU executor (oracle/_ref/ref_tool N); configs
+  3-5 also through size-independent properties (every Partial-free
+  destination shard equals the logical counter-hash tensor on its box);
 * the host-buffer (e2e) path and the Appendix-B1 rejection.
 """
 import random
@@ -161,6 +163,42 @@ def test_workload_full_size_vs_oracle(gpu_ctx, name):
     plan = H.classify(src, dst, shape, w.dtype)
     st = _gpu_case(gpu_ctx, plan, src, dst, shape, w.dtype, 1234, "real", w.n_virtual)
     assert st["hbm_write"] == st["dst_bytes"] or plan.json()["mid"] is not None
+
+
+@pytest.mark.parametrize("name", ["cfg3b", "cfg3a", "cfg3c", "cfg2a", "cfg2d", "cfg2e", "cfg2b",
+                                  "cfg2e:f32", "cfg3b:f32"])
+def test_workload_full_size_real_vs_native(gpu_ctx, name, tmp_path):
+    """Rounding- and order-sensitive parity at FULL size: real-valued payloads
+    through the reduction configs, every destination shard byte-compared with
+    the native CPU executor (oracle/_ref/ref_tool N, pinned to the numpy oracle
+    in test_native_oracle.py): ascending-id fp32 sums, one rounding per plan
+    phase, reproduced by the fused GPU program and by the plain register path.
+    In bf16 the rounding points decide the bits; the ":f32" variants (same
+    annotations, f32 storage) make the summation order decide them too."""
+    import native_ref
+    from paper_2504_20490_b200.executor import Program, ShardLayout
+    if not native_ref.available():
+        pytest.skip("oracle/_ref/ref_tool not built")
+    w = W.by_name(name.split(":")[0])
+    dtype = name.split(":")[1] if ":" in name else w.dtype
+    tid, src, dst, shape = w.transitions[0]
+    plan = H.classify(src, dst, shape, dtype)
+    _, want = native_ref.run(src, dst, shape, dtype, 4321, "real", 0, str(tmp_path))
+    mark = gpu_ctx.alloc(0)
+    try:
+        lay = ShardLayout(gpu_ctx, plan, w.n_virtual)
+        lay.fill_src(4321, "real")
+        for flags in (0, 2 | 4 | 8):
+            lay.clear_dst()
+            prog = Program(gpu_ctx, plan, lay, flags)
+            prog.run()
+            gpu_ctx.sync()
+            for (slot, dev) in lay.dst:
+                got = lay.read("dst", 0, dev).ravel()
+                assert np.array_equal(got.view(np.uint8), want[dev].view(np.uint8)), (name, flags, dev)
+            prog.close()
+    finally:
+        gpu_ctx.reset(mark)
 
 
 @pytest.mark.parametrize("name", ["cfg3b", "cfg3a", "cfg3c", "cfg2a", "cfg2d"])

@@ -36,7 +36,10 @@ def _gpus():
                                    # barriers as separate launches (default: folded into kernels)
                                    "67108864,67121152",
                                    # TMA bulk stores (to peers when pushed): alone, NO_SHARE, fan-out once
-                                   "33554432,33554560,33587200"])
+                                   "33554432,33554560,33587200",
+                                   # BASELINE reduction configs at FULL size, real-valued payloads,
+                                   # vs the native CPU executor: default, plain, pull-mid, fused
+                                   "full:0,14,12288,1"])
 def test_multi_gpu_parity(tmp_path, flags):
     n = int(os.environ.get("HS_TEST_RANKS", min(_gpus(), 8)))  # > GPUs: ranks share GPUs
     port = 29517 + sum(map(ord, flags)) % 300
@@ -47,9 +50,11 @@ def test_multi_gpu_parity(tmp_path, flags):
     env = dict(os.environ, HS_MGPU_OUT=out, HS_MGPU_FLAGS=flags.split(":")[-1])
     if flags.startswith("fine:"):
         env["HS_STREAM_CHUNK_KB"] = "1"
+    if flags.startswith("full:"):
+        env["HS_MGPU_FULL"] = "1"
     if flags.startswith("ce3:"):  # copy-engine relays in 3 chunks (uneven row cuts)
         env["HS_CE_CHUNKS"] = "3"
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = []
     for r in range(n):
