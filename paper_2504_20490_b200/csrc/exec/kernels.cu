@@ -546,6 +546,68 @@ __device__ void tma_signaller(const PhaseTables& t, SigRing* ring, int lane) {
   }
 }
 
+// TMA item record of item `i`, decoded by the producer warp from the task
+// descriptors (every lane returns its 16-byte word of the record: lanes 0-2
+// the TmaRecHead, lane 3 + k operand k).  `cur` is the warp's cursor into the
+// task table: items a CTA takes only ever increase, so the task is usually the
+// current one or the next; otherwise a binary search over TmaTask::item0
+// (L1-resident) finds it.  Called one item ahead, off the critical path.
+__device__ __forceinline__ int tma_find(const PhaseTables& t, int i, int cur) {
+  const TmaTask* tt = t.ttasks;
+  if (cur >= t.n_ttasks || __ldg(&tt[cur].item0) > i) cur = 0;
+  if (__ldg(&tt[cur + 1].item0) > i) return cur;
+  int lo = cur + 1, hi = t.n_ttasks - 1;  // largest k with item0 <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&tt[mid].item0) <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int kEs>
+__device__ __forceinline__ uint4 tma_record(const PhaseTables& t, int i, int lane, int& cur) {
+  cur = tma_find(t, i, cur);
+  const TmaTask* tk = t.ttasks + cur;
+  const int4 w0 = __ldg(reinterpret_cast<const int4*>(tk));      // item0, nterms, nout, ngroups
+  const int4 w1 = __ldg(reinterpret_cast<const int4*>(tk) + 1);  // wait, sig, need, mode
+  const int4 w2 = __ldg(reinterpret_cast<const int4*>(tk) + 2);  // n1, n2, row_vecs, per
+  const int4 w3 = __ldg(reinterpret_cast<const int4*>(tk) + 3);  // cpr, term0, out0, pad
+  const int j = i - w0.x;
+  const int n1 = w2.x, row_vecs = w2.z, per = w2.w, cpr = w3.x;
+  int pl, r, c, nrow, nvcol;
+  if (w1.w == 0) {  // row chunks
+    const int per_plane = n1 * cpr;
+    pl = j / per_plane;
+    const int rem = j - pl * per_plane;
+    r = rem / cpr;
+    c = (rem - r * cpr) * per;
+    nvcol = min(per, row_vecs - c);
+    nrow = 1;
+  } else {  // row runs
+    pl = j / cpr;
+    r = (j - pl * cpr) * per;
+    nrow = min(per, n1 - r);
+    c = 0;
+    nvcol = row_vecs;
+  }
+  if (lane == 0) return make_uint4(w0.y, w0.z, w0.w, nrow);
+  if (lane == 1) return make_uint4(nvcol, w1.x, w1.y, w1.z);
+  if (lane == 2) return __ldg(reinterpret_cast<const uint4*>(tk) + 4);  // gsize
+  const int k = lane - kTmaHeadWords, nterms = w0.y;
+  if (k >= nterms + w0.z) return make_uint4(0, 0, 0, 0);
+  const TermDesc* td = t.terms + (k < nterms ? w3.y + k : w3.z + (k - nterms));
+  const char* base = reinterpret_cast<const char*>(__ldg(reinterpret_cast<const unsigned long long*>(&td->base)));
+  const int64_t s0 = __ldg(&td->stride[0]), s1 = __ldg(&td->stride[1]), s2 = __ldg(&td->stride[2]);
+  const int n2 = w2.y;
+  const int i2 = pl % n2, i3 = pl / n2;
+  const unsigned long long row0 = reinterpret_cast<unsigned long long>(
+      base + kEs * (static_cast<int64_t>(r) * s0 + i2 * s1 + i3 * s2) + static_cast<int64_t>(c) * 16);
+  const unsigned long long step = static_cast<unsigned long long>(s0 * kEs);
+  return make_uint4(static_cast<unsigned>(row0), static_cast<unsigned>(row0 >> 32), static_cast<unsigned>(step),
+                    static_cast<unsigned>(step >> 32));
+}
+
 // Dynamic-schedule kernels: a CTA leaving the launch counts itself out; the
 // last one resets the scheduler words for the program's next run.
 __device__ __forceinline__ void sched_retire(const PhaseTables& t) {
@@ -738,9 +800,10 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
     };
     int it = resolve(lane == 0 ? issue() : 0);
     uint4 next = make_uint4(0, 0, 0, 0);
+    int cursor = 0;  // task-table cursor of tma_record (warp-uniform)
     int pend = 0;
     if (it < t.n_items) {
-      if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+      next = tma_record<sizeof(T)>(t, it, lane, cursor);
       if (lane == 0) pend = issue();
     }
     for (int iter = 0;; ++iter) {
@@ -749,7 +812,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
       if (cur_it < t.n_items) {
         it = resolve(pend);
         if (it < t.n_items) {
-          if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+          next = tma_record<sizeof(T)>(t, it, lane, cursor);
           if (lane == 0) pend = issue();
         }
       }
@@ -890,14 +953,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
     };
     int it = next_item(-1, 0);
     uint4 next = make_uint4(0, 0, 0, 0);
-    if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+    int cursor = 0;  // task-table cursor of tma_record (warp-uniform)
+    if (it < t.n_items) next = tma_record<sizeof(T)>(t, it, lane, cursor);
     for (int iter = 0;; ++iter) {
       const int cur_it = it;
       const uint4 cur = next;
       if (cur_it < t.n_items) {
         const int nxt = next_item(cur_it, iter + 1);
         it = nxt;
-        if (nxt < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nxt) * W + lane];
+        if (nxt < t.n_items) next = tma_record<sizeof(T)>(t, nxt, lane, cursor);
       }
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
@@ -974,11 +1038,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     int iter = 0;
     int it = blockIdx.x;
     uint4 next = make_uint4(0, 0, 0, 0);
-    if (it < t.n_items && lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
+    int cursor = 0;  // task-table cursor of tma_record (warp-uniform)
+    if (it < t.n_items) next = tma_record<sizeof(T)>(t, it, lane, cursor);
     for (; it < t.n_items; it += gridDim.x, ++iter) {
       const uint4 cur = next;
       const int nit = it + gridDim.x;
-      if (nit < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nit) * W + lane];
+      if (nit < t.n_items) next = tma_record<sizeof(T)>(t, nit, lane, cursor);
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
       uint4* m = meta + s * 32;

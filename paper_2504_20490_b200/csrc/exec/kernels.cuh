@@ -48,9 +48,12 @@ struct WorkItem {
   int32_t nvcol;
 };
 
-// TMA-path item record, built on the host so the producer warp fetches one
-// fixed-size slot per item (no dependent descriptor loads):
-//   TmaRecHead, then (nterms + nout) TmaOperand: terms first, then outputs.
+// TMA-path item record as the producer warp stages it in shared memory for
+// the consumers: TmaRecHead, then (nterms + nout) TmaOperand (terms first,
+// then outputs).  The producer DECODES it from the item index (tma_record in
+// kernels.cu): TMA tasks own contiguous item ranges (TmaTask::item0), so the
+// host builds one TmaTask per box task, never a per-item table -- a cfg4
+// switch compiles 1034 descriptors instead of 445k records.
 struct TmaRecHead {
   int32_t nterms, nout, ngroups, nrow;
   int32_t nvcol;
@@ -64,6 +67,26 @@ struct TmaOperand {
   int64_t step;  // bytes between rows
 };
 inline constexpr int kTmaHeadWords = sizeof(TmaRecHead) / 16;                 // 3
+
+// A TMA box task: the item geometry and the record fields that do not vary
+// by item.  Items [item0, next task's item0) cut the task's (plane, row) space
+// into either row chunks (mode 0: one row, `per` vectors per item, `cpr`
+// items per row) or row runs (mode 1: `per` whole rows per item, `cpr` items
+// per plane); planes are (dim2, dim3) pairs, dim2 of extent n2.
+struct TmaTask {
+  int32_t item0;               // first item of the task in launch order
+  int32_t nterms, nout, ngroups;
+  int32_t wait, sig, need;     // as TmaRecHead
+  int32_t mode;                // 0 row chunks, 1 row runs
+  int32_t n1, n2;              // rows per plane, dim-2 extent
+  int32_t row_vecs;            // 16-byte vectors per row
+  int32_t per;                 // mode 0: vectors per item; mode 1: rows per item
+  int32_t cpr;                 // mode 0: items per row; mode 1: items per plane
+  int32_t term0, out0;         // operands in PhaseTables::terms
+  int32_t pad;
+  uint8_t gsize[16];
+};
+static_assert(sizeof(TmaTask) == 80, "TmaTask layout");
 inline constexpr int kTmaMaxWords = kTmaHeadWords + kMaxTerms + kMaxOuts;    // 27 <= 32 lanes
 
 // Streamed launches (both plan phases in one launch, no barrier between):
@@ -82,11 +105,12 @@ struct PhaseTables {
   const TaskDesc* tasks;
   const TermDesc* terms;
   const WorkItem* items;  // register path
-  const uint4* recs;      // TMA path: n_items slots of rec_words 16-byte words
+  const TmaTask* ttasks;   // TMA path: n_ttasks descriptors in item order
+  int32_t n_ttasks;
   int* sched;             // TMA path: {next first-queue item, finished CTAs, next second-queue
                           // item, pad}; zero between launches
   int32_t n_items;
-  int32_t rec_words;
+  int32_t rec_words;      // TMA path: 16-byte words of the widest record of the launch
   int32_t n_static;       // TMA path: items [0, n_static) are dealt round-robin
   // TMA path queues: items [0, n_first) never wait; [n_first, n_items) may.
   // CTAs [0, first_ctas) drain the first queue, then the second; the others

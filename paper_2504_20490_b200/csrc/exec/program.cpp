@@ -20,6 +20,8 @@
 //   * output merging: tasks with identical inputs (replicas, SplitAG fan-out)
 //     become one task with several outputs, so inputs are read once.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -40,6 +42,12 @@ namespace {
 constexpr int64_t kItemBytes = 64 * 1024;     // register path, output bytes per item
 constexpr int64_t kTmaItemBytes = 32 * 1024;  // TMA path upper bound (also <= stage / nterms)
 constexpr int kBlocksPerSm = 2;
+
+// Host-side item geometry of one TMA task (TmaTask minus the record fields).
+struct TmaGeom {
+  int32_t task, mode, per, cpr;
+  int64_t count;
+};
 constexpr int kSlots = 9;
 // HS_PROG_BULK_STORE: a copy's outputs stored by TMA bulk stores (the rest from
 // registers, so the TMA unit still has room for the loads feeding the stages)
@@ -124,6 +132,7 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
     add_state(static_cast<int>(states_.size()) - 1, t, *annos[t].second, dst_off);
   }
   if (has_mid) add_state(1, 0, *comm->mid, nullptr);
+  clock_.mark("placements");
 
   for (const auto& [key, L] : states_[0])
     if (L.rank == ctx_.rank() && L.offset != SIZE_MAX) {
@@ -307,6 +316,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     n_phases_ = 1;
   }
   stats_.plan_phases = n_phases_;
+  clock_.mark("lowering");
 
   // ---- rewrites (results are bit-identical by construction; see header)
   nccl_mode_ = ctx_.world() > 1 && (flags_ & HS_PROG_NCCL);
@@ -379,6 +389,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     tasks = fanout_once(std::move(tasks));
   if (nccl_mode_) stage_for_nccl(tasks);
   if (ce_mode_ && ce_copies_.empty()) ce_mode_ = false;  // no relay to move
+  clock_.mark("rewrites");
 
   // world > 1: both plan phases in one launch with per-chunk ready flags
   // (kept only if every producer / consumer piece runs on the TMA path).
@@ -503,6 +514,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     if (c.receiver == me) stats_.nvlink_in += b;
   }
   if (ctx_.is_analysis()) analysed_ = mine;
+  clock_.mark("accounting");
   for (const BoxTask& t : mine) {
     for (const Operand& o : t.dsts)
       if (loc(o.state, t.tensor, o.dev).offset == SIZE_MAX)
@@ -512,6 +524,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
         fail(Errc::MissingShard, "source shard of device " + std::to_string(o.dev) + " has no buffer");
   }
   build_tables(mine);
+  clock_.mark("tables");
   if (ce_mode_ && !ctx_.is_analysis()) ce_build();
 }
 
@@ -1345,14 +1358,22 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     std::vector<TaskDesc> tasks;
     std::vector<TermDesc> terms;
     std::vector<const BoxTask*> src;  // the BoxTask of each TaskDesc
-    // [0] TMA; [1..4] register copy/zero by width 16, 8, 4, 2; [5..8] register reduce
+    // [0] unused (TMA items are decoded from `tma`); [1..4] register copy/zero by
+    // width 16, 8, 4, 2; [5..8] register reduce
     std::vector<WorkItem> items[kSlots];
+    std::vector<TmaGeom> tma;  // TMA tasks in launch (queue) order
+    int64_t tma_items() const {
+      int64_t n = 0;
+      for (const TmaGeom& g : tma) n += g.count;
+      return n;
+    }
   };
   auto slot_of = [](int vb, bool tma, bool reduce) {
     return tma ? 0 : (vb == 16 ? 1 : vb == 8 ? 2 : vb == 4 ? 3 : 4) + (reduce ? 4 : 0);
   };
   std::vector<Host> ph(n_phases_);
   stats_.phases = n_phases_;
+  clock_.mark("tables:init");
 
   for (const BoxTask& bt : tasks) {
     Host& H = ph.at(bt.phase);
@@ -1401,6 +1422,25 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     }
     const int64_t target = std::max<int64_t>(1, item_bytes / vb);
     const int64_t planes = static_cast<int64_t>(td.n[2]) * td.n[3];
+    if (tma) {
+      // TMA items are decoded on the device from the task (kernels.cu
+      // tma_record): only the geometry is recorded here.
+      TmaGeom g{task_id, 0, 0, 0, 0};
+      if (row_vecs >= target) {
+        g.mode = 0;
+        g.per = static_cast<int32_t>(target);
+        g.cpr = static_cast<int32_t>((row_vecs + target - 1) / target);
+        g.count = planes * td.n[1] * g.cpr;
+      } else {
+        g.mode = 1;
+        g.per = static_cast<int32_t>(std::max<int64_t>(1, target / row_vecs));
+        g.cpr = (td.n[1] + g.per - 1) / g.per;
+        g.count = planes * g.cpr;
+      }
+      if (g.count > INT32_MAX) fail(Errc::UnsupportedOp, "more than 2^31 items in one task");
+      H.tma.push_back(g);
+      continue;
+    }
     std::vector<WorkItem>& items = H.items[slot_of(vb, tma, td.nterms >= 2)];
     for (int64_t pl = 0; pl < planes; ++pl) {
       if (row_vecs >= target) {
@@ -1417,6 +1457,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     }
   }
 
+  clock_.mark("items");
   // Streamed launches: signalling tasks' SigDescs and flag addresses; TMA
   // items reordered into the two queues (signalling work first, then other
   // non-waiting work; then waiting work), each by the piece's position along
@@ -1429,29 +1470,29 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   for (int p = 0; p < n_phases_; ++p) {
     Host& H = ph[p];
     task_sig[p].assign(H.tasks.size(), -1);
+    if (H.tma_items() > INT32_MAX) fail(Errc::UnsupportedOp, "more than 2^31 TMA items in one launch");
     if (!streamed_) {
-      n_first[p] = static_cast<int32_t>(H.items[0].size());
+      n_first[p] = static_cast<int32_t>(H.tma_items());
       continue;
     }
-    std::vector<int64_t> cnt(H.tasks.size(), 0);
-    for (const WorkItem& w : H.items[0]) cnt[w.task] += 1;
-    for (size_t k = 0; k < H.tasks.size(); ++k) {
-      const BoxTask& bt = *H.src[k];
-      if (bt.targets.empty() || cnt[k] == 0) continue;
-      task_sig[p][k] = static_cast<int32_t>(sigs.size());
-      sigs.push_back({static_cast<uint32_t>(sigs.size()), static_cast<uint32_t>(cnt[k]),
+    for (const TmaGeom& g : H.tma) {
+      const BoxTask& bt = *H.src[g.task];
+      if (bt.targets.empty() || g.count == 0) continue;
+      task_sig[p][g.task] = static_cast<int32_t>(sigs.size());
+      sigs.push_back({static_cast<uint32_t>(sigs.size()), static_cast<uint32_t>(g.count),
                       static_cast<uint32_t>(targets.size()), static_cast<uint32_t>(bt.targets.size())});
       for (const auto& [r, flag] : bt.targets)
         targets.push_back(reinterpret_cast<unsigned int*>(ctx_.arena_of(r) + flag_off_) + flag);
     }
-    auto rank_key = [&](const WorkItem& w) {
-      const BoxTask& bt = *H.src[w.task];
+    auto rank_key = [&](const TmaGeom& g) {
+      const BoxTask& bt = *H.src[g.task];
       const int queue = bt.wait >= 0 ? 2 : bt.targets.empty() ? 1 : 0;
       const double pos = static_cast<double>(bt.box.bounds[0][0]) / std::max<int64_t>(1, shapes_[bt.tensor][0]);
       return std::make_pair(queue, pos);
     };
-    std::stable_sort(H.items[0].begin(), H.items[0].end(),
-                     [&](const WorkItem& a, const WorkItem& b) { return rank_key(a) < rank_key(b); });
+    // tasks (each a contiguous run of items) into the two queues
+    std::stable_sort(H.tma.begin(), H.tma.end(),
+                     [&](const TmaGeom& a, const TmaGeom& b) { return rank_key(a) < rank_key(b); });
     // CTAs of the first queue in proportion to its modelled time (HBM bytes
     // at 6.5 TB/s vs NVLink bytes at 0.77 TB/s, whichever binds).
     double hbm[2] = {0, 0}, nv[2] = {0, 0};
@@ -1462,55 +1503,50 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       for (const auto* ops : {&bt.dsts, &bt.terms})
         for (const Operand& o : *ops) (loc(o.state, bt.tensor, o.dev).rank == bt.rank ? hbm : nv)[q] += bytes;
     }
-    for (const WorkItem& w : H.items[0]) n_first[p] += H.src[w.task]->wait < 0 ? 1 : 0;
+    for (const TmaGeom& g : H.tma) n_first[p] += H.src[g.task]->wait < 0 ? static_cast<int32_t>(g.count) : 0;
     const double t0 = std::max(hbm[0] / 6.5e12, nv[0] / 7.7e11), t1 = std::max(hbm[1] / 6.5e12, nv[1] / 7.7e11);
     first_frac[p] = t0 + t1 > 0 ? t0 / (t0 + t1) : 1.0;
     if (const int share = (flags_ >> 16) & 0xff) first_frac[p] = share / 64.0;
   }
 
-  // TMA item records: header + every operand's first-row address, one
-  // fixed-size slot per item so the producer warp never chases descriptors.
-  std::vector<std::vector<uint4>> recs(n_phases_);
+  clock_.mark("queues");
+  // TMA task descriptors in item order (+ a sentinel whose item0 is the item
+  // count); the producer warp decodes every item's record from them.
+  std::vector<std::vector<TmaTask>> ttasks(n_phases_);
   std::vector<int> rec_words(n_phases_, kTmaHeadWords);
   for (int p = 0; p < n_phases_; ++p) {
     const Host& H = ph[p];
-    for (const WorkItem& w : H.items[0]) {
-      const TaskDesc& td = H.tasks[w.task];
+    int64_t item0 = 0;
+    for (const TmaGeom& g : H.tma) {
+      const TaskDesc& td = H.tasks[g.task];
+      const BoxTask& bt = *H.src[g.task];
       rec_words[p] = std::max(rec_words[p], kTmaHeadWords + td.nterms + td.nout);
+      TmaTask tt{};
+      tt.item0 = static_cast<int32_t>(item0);
+      tt.nterms = td.nterms;
+      tt.nout = td.nout;
+      tt.ngroups = td.ngroups;
+      tt.wait = bt.wait;
+      tt.sig = task_sig[p][g.task];
+      tt.need = bt.need;
+      tt.mode = g.mode;
+      tt.n1 = td.n[1];
+      tt.n2 = td.n[2];
+      tt.row_vecs = static_cast<int32_t>(static_cast<int64_t>(td.n[0]) * es_ / 16);
+      tt.per = g.per;
+      tt.cpr = g.cpr;
+      tt.term0 = td.term0;
+      tt.out0 = td.out0;
+      std::memcpy(tt.gsize, td.gsize, sizeof(tt.gsize));
+      ttasks[p].push_back(tt);
+      item0 += g.count;
     }
-    const int W = rec_words[p];
-    recs[p].assign(H.items[0].size() * W, make_uint4(0, 0, 0, 0));
-    for (size_t i = 0; i < H.items[0].size(); ++i) {
-      const WorkItem& w = H.items[0][i];
-      const TaskDesc& td = H.tasks[w.task];
-      const BoxTask& bt = *H.src[w.task];
-      uint4* slot = recs[p].data() + i * W;
-      TmaRecHead head{};
-      head.nterms = td.nterms;
-      head.nout = td.nout;
-      head.ngroups = td.ngroups;
-      head.nrow = w.nrow;
-      head.nvcol = w.nvcol;
-      head.wait = bt.wait;
-      head.sig = task_sig[p][w.task];
-      head.need = bt.need;
-      std::memcpy(head.gsize, td.gsize, sizeof(head.gsize));
-      std::memcpy(slot, &head, sizeof(head));
-      const int64_t i2 = w.plane % td.n[2], i3 = w.plane / td.n[2];
-      auto operand = [&](const TermDesc& t) {
-        TmaOperand op;
-        op.row0 = const_cast<char*>(t.base) +
-                  es_ * (w.row0 * t.stride[0] + i2 * t.stride[1] + i3 * t.stride[2]) +
-                  static_cast<int64_t>(w.vcol0) * 16;
-        op.step = t.stride[0] * es_;
-        return op;
-      };
-      TmaOperand* ops = reinterpret_cast<TmaOperand*>(slot + kTmaHeadWords);
-      for (int k = 0; k < td.nterms; ++k) ops[k] = operand(H.terms[td.term0 + k]);
-      for (int o = 0; o < td.nout; ++o) ops[td.nterms + o] = operand(H.terms[td.out0 + o]);
-    }
+    TmaTask sentinel{};
+    sentinel.item0 = static_cast<int32_t>(item0);
+    ttasks[p].push_back(sentinel);
   }
 
+  clock_.mark("records");
   // One device block for every phase's tables.
   size_t total = 0;
   auto reserve = [&total](size_t bytes) {
@@ -1519,14 +1555,14 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     return off;
   };
   struct Offs {
-    size_t tasks, terms, items[kSlots], recs, sched;
+    size_t tasks, terms, items[kSlots], ttasks, sched;
   };
   std::vector<Offs> offs(n_phases_);
   for (int p = 0; p < n_phases_; ++p) {
     offs[p].tasks = reserve(ph[p].tasks.size() * sizeof(TaskDesc));
     offs[p].terms = reserve(ph[p].terms.size() * sizeof(TermDesc));
     for (int v = 0; v < kSlots; ++v) offs[p].items[v] = reserve(ph[p].items[v].size() * sizeof(WorkItem));
-    offs[p].recs = reserve(recs[p].size() * sizeof(uint4));
+    offs[p].ttasks = reserve(ttasks[p].size() * sizeof(TmaTask));
     offs[p].sched = reserve(4 * sizeof(int));  // zero-initialised scheduler words
   }
   const size_t sigs_off = reserve(sigs.size() * sizeof(SigDesc));
@@ -1539,10 +1575,11 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     for (int v = 0; v < kSlots; ++v)
       std::memcpy(host.data() + offs[p].items[v], ph[p].items[v].data(),
                   ph[p].items[v].size() * sizeof(WorkItem));
-    std::memcpy(host.data() + offs[p].recs, recs[p].data(), recs[p].size() * sizeof(uint4));
+    std::memcpy(host.data() + offs[p].ttasks, ttasks[p].data(), ttasks[p].size() * sizeof(TmaTask));
   }
   std::memcpy(host.data() + sigs_off, sigs.data(), sigs.size() * sizeof(SigDesc));
   std::memcpy(host.data() + targets_off, targets.data(), targets.size() * sizeof(unsigned int*));
+  clock_.mark("pack");
   char* base = nullptr;
   if (!ctx_.is_analysis()) {
     cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
@@ -1550,6 +1587,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
                "cudaMemcpy(tables)");
     base = static_cast<char*>(dev_block_);
   }
+  clock_.mark("upload");
   dphases_.assign(n_phases_, {});
   const int max_grid = ctx_.sm_count() * kBlocksPerSm;
   int launches = 0;
@@ -1557,7 +1595,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     DevicePhase& d = dphases_[p];
     int64_t n = 0;
     for (int v = 0; v < kSlots; ++v) {
-      const int32_t cnt = static_cast<int32_t>(ph[p].items[v].size());
+      const int32_t cnt = static_cast<int32_t>(v == 0 ? ph[p].tma_items() : ph[p].items[v].size());
       n += cnt;
       if (!cnt) continue;
       Launch l;
@@ -1565,7 +1603,8 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables.tasks = reinterpret_cast<TaskDesc*>(base + offs[p].tasks);
       l.tables.terms = reinterpret_cast<TermDesc*>(base + offs[p].terms);
       l.tables.items = reinterpret_cast<WorkItem*>(base + offs[p].items[v]);
-      l.tables.recs = reinterpret_cast<const uint4*>(base + offs[p].recs);
+      l.tables.ttasks = reinterpret_cast<const TmaTask*>(base + offs[p].ttasks);
+      l.tables.n_ttasks = static_cast<int32_t>(ttasks[p].size()) - 1;
       l.tables.sched = reinterpret_cast<int*>(base + offs[p].sched);
       l.tables.n_items = cnt;
       l.tables.rec_words = rec_words[p];

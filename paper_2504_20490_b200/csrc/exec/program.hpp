@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <memory>
@@ -16,6 +19,18 @@
 #include "kernels.cuh"
 
 namespace hshard::exec {
+
+// HS_COMPILE_TRACE=1: per-stage compile times on stderr (cold-switch analysis).
+struct StageClock {
+  bool on = std::getenv("HS_COMPILE_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[compile] %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 void cuda_check(cudaError_t e, const char* what);
 
@@ -262,6 +277,7 @@ class Program {
   cudaEvent_t host_ev_[3] = {nullptr, nullptr, nullptr};  // run_host_async: inputs landed / run done / read
   size_t events_used_ = 0;
   ProgramStats stats_;
+  StageClock clock_;
   std::vector<BoxTask> analysed_;  // analysis contexts: this rank's final tasks
   // host-buffer path: (virtual device, tensor) -> (offset, bytes) on this rank
   std::vector<std::tuple<DeviceId, int, size_t, size_t>> host_src_, host_dst_;

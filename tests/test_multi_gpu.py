@@ -61,6 +61,11 @@ def test_multi_gpu_parity(tmp_path, flags):
         with open(f"{out}.{r}") as f:
             lines.append(json.loads(f.read()))
     assert len(lines) == n, (res.stdout[-2000:], res.stderr[-2000:])
+    for l in lines:  # one summary line per (rank, case, flags): committed as the parity log
+        for c in l["cases"]:
+            print(f"rank {l['rank']}/{n} " + json.dumps({k: c.get(k) for k in ("case", "flags", "bad", "skipped",
+                                                                            "nvlink_in", "nvlink_out", "streamed")
+                                                      if k in c}))
     for l in lines:
         assert l["ok"], json.dumps(l)[:3000]
     # every byte pulled over NVLink by one rank is served by another
