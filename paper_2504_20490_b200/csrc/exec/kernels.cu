@@ -546,12 +546,14 @@ __device__ void tma_signaller(const PhaseTables& t, SigRing* ring, int lane) {
   }
 }
 
-// TMA item record of item `i`, decoded by the producer warp from the task
-// descriptors (every lane returns its 16-byte word of the record: lanes 0-2
-// the TmaRecHead, lane 3 + k operand k).  `cur` is the warp's cursor into the
-// task table: items a CTA takes only ever increase, so the task is usually the
-// current one or the next; otherwise a binary search over TmaTask::item0
-// (L1-resident) finds it.  Called one item ahead, off the critical path.
+// TMA item record of item `i`, decoded from the task descriptors (every lane
+// returns its 16-byte word of the record: lanes 0-2 the TmaRecHead, lane 3 + k
+// operand k).  `cur` is the warp's cursor into the task table: consecutive
+// items are usually in the current task or the next; otherwise a binary
+// search over TmaTask::item0 finds it.
+// Used by expand_records_kernel, once per compiled program: the phase kernels
+// keep reading one prefetched record word per lane (a dependent decode in the
+// producer warp measured 6-40% slower: it stalls the warp that issues the TMA).
 __device__ __forceinline__ int tma_find(const PhaseTables& t, int i, int cur) {
   const TmaTask* tt = t.ttasks;
   if (cur >= t.n_ttasks || __ldg(&tt[cur].item0) > i) cur = 0;
@@ -606,6 +608,19 @@ __device__ __forceinline__ uint4 tma_record(const PhaseTables& t, int i, int lan
   const unsigned long long step = static_cast<unsigned long long>(s0 * kEs);
   return make_uint4(static_cast<unsigned>(row0), static_cast<unsigned>(row0 >> 32), static_cast<unsigned>(step),
                     static_cast<unsigned>(step >> 32));
+}
+
+// Expands a launch's records from its task descriptors on the device, one
+// warp per item (grid-stride): what the host used to build item by item.
+template <int kEs>
+__global__ void __launch_bounds__(256) expand_records_kernel(PhaseTables t, uint4* recs, int W) {
+  const int lane = threadIdx.x & 31;
+  const int warps = static_cast<int>(gridDim.x * blockDim.x) >> 5;
+  int cur = 0;
+  for (int i = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < t.n_items; i += warps) {
+    const uint4 w = tma_record<kEs>(t, i, lane, cur);
+    if (lane < W) recs[static_cast<size_t>(i) * W + lane] = w;
+  }
 }
 
 // Dynamic-schedule kernels: a CTA leaving the launch counts itself out; the
@@ -800,10 +815,9 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
     };
     int it = resolve(lane == 0 ? issue() : 0);
     uint4 next = make_uint4(0, 0, 0, 0);
-    int cursor = 0;  // task-table cursor of tma_record (warp-uniform)
     int pend = 0;
     if (it < t.n_items) {
-      next = tma_record<sizeof(T)>(t, it, lane, cursor);
+      if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
       if (lane == 0) pend = issue();
     }
     for (int iter = 0;; ++iter) {
@@ -812,7 +826,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
       if (cur_it < t.n_items) {
         it = resolve(pend);
         if (it < t.n_items) {
-          next = tma_record<sizeof(T)>(t, it, lane, cursor);
+          if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
           if (lane == 0) pend = issue();
         }
       }
@@ -953,15 +967,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
     };
     int it = next_item(-1, 0);
     uint4 next = make_uint4(0, 0, 0, 0);
-    int cursor = 0;  // task-table cursor of tma_record (warp-uniform)
-    if (it < t.n_items) next = tma_record<sizeof(T)>(t, it, lane, cursor);
+    if (it < t.n_items) if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
     for (int iter = 0;; ++iter) {
       const int cur_it = it;
       const uint4 cur = next;
       if (cur_it < t.n_items) {
         const int nxt = next_item(cur_it, iter + 1);
         it = nxt;
-        if (nxt < t.n_items) next = tma_record<sizeof(T)>(t, nxt, lane, cursor);
+        if (nxt < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nxt) * W + lane];
       }
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
@@ -1038,12 +1051,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     int iter = 0;
     int it = blockIdx.x;
     uint4 next = make_uint4(0, 0, 0, 0);
-    int cursor = 0;  // task-table cursor of tma_record (warp-uniform)
-    if (it < t.n_items) next = tma_record<sizeof(T)>(t, it, lane, cursor);
+    if (it < t.n_items) if (lane < W) next = t.recs[static_cast<size_t>(it) * W + lane];
     for (; it < t.n_items; it += gridDim.x, ++iter) {
       const uint4 cur = next;
       const int nit = it + gridDim.x;
-      if (nit < t.n_items) next = tma_record<sizeof(T)>(t, nit, lane, cursor);
+      if (nit < t.n_items && lane < W) next = t.recs[static_cast<size_t>(nit) * W + lane];
       const int s = iter % kTmaStages;
       if (iter >= kTmaStages) mbar_wait(&empty[s], ((iter / kTmaStages) + 1) & 1);
       uint4* m = meta + s * 32;
@@ -1352,6 +1364,19 @@ struct VerifyK {
 }  // namespace
 
 int tma_grid(int sm_count) { return sm_count; }
+
+cudaError_t launch_expand_records(const PhaseTables& t, int dtype, uint4* recs, int rec_words, int sm_count,
+                                  cudaStream_t s) {
+  if (t.n_items == 0) return cudaSuccess;
+  const int blocks = std::max(1, std::min(sm_count * 8, (t.n_items + 7) / 8));
+  switch (dtype) {
+    case 0: case 2: expand_records_kernel<4><<<blocks, 256, 0, s>>>(t, recs, rec_words); break;
+    case 1: case 3: expand_records_kernel<8><<<blocks, 256, 0, s>>>(t, recs, rec_words); break;
+    case 4: expand_records_kernel<2><<<blocks, 256, 0, s>>>(t, recs, rec_words); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, bool reduce,
                          int grid, cudaStream_t s) {

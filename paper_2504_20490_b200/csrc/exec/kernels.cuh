@@ -48,12 +48,14 @@ struct WorkItem {
   int32_t nvcol;
 };
 
-// TMA-path item record as the producer warp stages it in shared memory for
-// the consumers: TmaRecHead, then (nterms + nout) TmaOperand (terms first,
-// then outputs).  The producer DECODES it from the item index (tma_record in
-// kernels.cu): TMA tasks own contiguous item ranges (TmaTask::item0), so the
-// host builds one TmaTask per box task, never a per-item table -- a cfg4
-// switch compiles 1034 descriptors instead of 445k records.
+// TMA-path item record, one fixed-size slot per item so the producer warp
+// fetches one 16-byte word per lane, prefetched an item ahead (no dependent
+// descriptor loads on its critical path): TmaRecHead, then (nterms + nout)
+// TmaOperand (terms first, then outputs).  The host builds only one TmaTask
+// per box task (TMA tasks own contiguous item ranges, TmaTask::item0); the
+// records are expanded from them on the device at compile time
+// (launch_expand_records) -- a cfg4 switch uploads 1034 descriptors instead of
+// building 445k records on the host.
 struct TmaRecHead {
   int32_t nterms, nout, ngroups, nrow;
   int32_t nvcol;
@@ -105,8 +107,9 @@ struct PhaseTables {
   const TaskDesc* tasks;
   const TermDesc* terms;
   const WorkItem* items;  // register path
-  const TmaTask* ttasks;   // TMA path: n_ttasks descriptors in item order
-  int32_t n_ttasks;
+  const uint4* recs;      // TMA path: n_items slots of rec_words 16-byte words
+  const TmaTask* ttasks;  // TMA path: n_ttasks descriptors in item order (+ sentinel); the
+  int32_t n_ttasks;       // source launch_expand_records expands `recs` from
   int* sched;             // TMA path: {next first-queue item, finished CTAs, next second-queue
                           // item, pad}; zero between launches
   int32_t n_items;
@@ -147,6 +150,10 @@ inline constexpr int kStageBytes = 48 * 1024;
 cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tma, bool reduce,
                          int grid, cudaStream_t s);
 int tma_grid(int sm_count);
+// Writes the launch's TMA item records (t.recs, t.rec_words words each) from
+// its task descriptors (t.ttasks), on the device.
+cudaError_t launch_expand_records(const PhaseTables& t, int dtype, uint4* recs, int rec_words, int sm_count,
+                                  cudaStream_t s);
 
 // Counter-hash payload generator (mirror of oracle/datagen.py).
 struct FillDesc {

@@ -1555,7 +1555,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     return off;
   };
   struct Offs {
-    size_t tasks, terms, items[kSlots], ttasks, sched;
+    size_t tasks, terms, items[kSlots], ttasks, recs, sched;
   };
   std::vector<Offs> offs(n_phases_);
   for (int p = 0; p < n_phases_; ++p) {
@@ -1568,7 +1568,12 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   const size_t sigs_off = reserve(sigs.size() * sizeof(SigDesc));
   const size_t targets_off = reserve(targets.size() * sizeof(unsigned int*));
   const size_t done_off = reserve(sigs.size() * sizeof(unsigned long long));  // zero: no items done yet
-  std::vector<char> host(std::max<size_t>(total, 1));
+  // The TMA records are written on the device (expanded from the task
+  // descriptors below): reserved after everything that is uploaded.
+  const size_t upload = total;
+  for (int p = 0; p < n_phases_; ++p)
+    offs[p].recs = reserve(static_cast<size_t>(ph[p].tma_items()) * rec_words[p] * sizeof(uint4));
+  std::vector<char> host(std::max<size_t>(upload, 1));
   for (int p = 0; p < n_phases_; ++p) {
     std::memcpy(host.data() + offs[p].tasks, ph[p].tasks.data(), ph[p].tasks.size() * sizeof(TaskDesc));
     std::memcpy(host.data() + offs[p].terms, ph[p].terms.data(), ph[p].terms.size() * sizeof(TermDesc));
@@ -1582,7 +1587,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   clock_.mark("pack");
   char* base = nullptr;
   if (!ctx_.is_analysis()) {
-    cuda_check(cudaMalloc(&dev_block_, host.size()), "cudaMalloc(tables)");
+    cuda_check(cudaMalloc(&dev_block_, std::max<size_t>(total, 1)), "cudaMalloc(tables)");
     cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
                "cudaMemcpy(tables)");
     base = static_cast<char*>(dev_block_);
@@ -1604,6 +1609,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables.terms = reinterpret_cast<TermDesc*>(base + offs[p].terms);
       l.tables.items = reinterpret_cast<WorkItem*>(base + offs[p].items[v]);
       l.tables.ttasks = reinterpret_cast<const TmaTask*>(base + offs[p].ttasks);
+      l.tables.recs = reinterpret_cast<const uint4*>(base + offs[p].recs);
       l.tables.n_ttasks = static_cast<int32_t>(ttasks[p].size()) - 1;
       l.tables.sched = reinterpret_cast<int*>(base + offs[p].sched);
       l.tables.n_items = cnt;
@@ -1622,6 +1628,10 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
         stats_.trace_ctas = l.grid;
         l.tables.trace = reinterpret_cast<unsigned long long*>(ctx_.arena() + stats_.trace_off);
       }
+      if (l.tma && !ctx_.is_analysis())
+        cuda_check(launch_expand_records(l.tables, dtype_, const_cast<uint4*>(l.tables.recs), l.tables.rec_words,
+                                         ctx_.sm_count(), ctx_.stream()),
+                   "expand records");
       if (l.tma) {
         stats_.tma_items += cnt;
         if (streamed_) {
@@ -1670,6 +1680,8 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }
+  // the records are complete before any stream can run the program
+  if (!ctx_.is_analysis()) cuda_check(cudaStreamSynchronize(ctx_.stream()), "expand records sync");
   int barriers = ctx_.world() > 1 && !nccl_mode_ ? n_phases_ + (remote_final_writes_ ? 1 : 0) : 0;
   for (const DevicePhase& d : dphases_) barriers -= d.fold_barrier ? 1 : 0;
   stats_.kernels_per_run = launches + barriers;
