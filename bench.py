@@ -271,6 +271,70 @@ def reference_arm(args, w, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- graph switches
+def switch_latency(ctx, stream, steps, cycles, allreduce_max, barrier, warm_runs=10):
+    """SPEC.md:419-433 graph switching end to end, per step of a strategy cycle
+    (executor.StrategyCycle): plan_switch (host) -> compile (host tables + device record
+    expansion) -> first run, then warm runs of the same program.  Cycle 1 is cold; later
+    cycles hit the SwitchCache (plans and programs per (src, dst) strategy).  The first
+    state holds the counter-hash tensors and every state is verified on-device against
+    them, so the round trip back to the first strategy is checked bit-exactly."""
+    import torch
+    from paper_2504_20490_b200 import hshard as H
+    from paper_2504_20490_b200.executor import StrategyCycle
+    sp = stream.cuda_stream
+    ctx.reset(0)
+    try:
+        cyc_obj = StrategyCycle(ctx, [w.transitions for w in steps], steps[0].dtype, steps[0].n_virtual)
+    except H.HshardError as e:
+        return {"skipped": str(e)[:200]}
+    seed = 5
+    cyc_obj.states[0].fill(seed, "grid", sp)
+    stream.synchronize()
+    ctx.sync()
+    out = []
+    for cyc in range(cycles):
+        for k, w in enumerate(steps):
+            barrier()
+            t0 = time.perf_counter()
+            prog, info = cyc_obj.prepare(k)
+            t2 = time.perf_counter()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record()
+                prog.run(sp)
+                b.record()
+            b.synchronize()
+            ctx.sync()
+            t3 = time.perf_counter()
+            bad = cyc_obj.states[k + 1].verify(seed)
+            rec = {"step": w.name, "cycle": cyc, "plan_cached": info["plan_cached"],
+                   "program_cached": info["program_cached"], "plan_ms": allreduce_max(info["plan_ms"]),
+                   "compile_ms": allreduce_max(info["compile_ms"]), "first_run_ms": allreduce_max((t3 - t2) * 1e3),
+                   "first_run_device_ms": allreduce_max(a.elapsed_time(b)),
+                   "total_ms": allreduce_max((t3 - t0) * 1e3),
+                   "verified": bool(allreduce_max(float(bad)) == 0)}
+            if cyc == cycles - 1:  # warm: the cached program, device time per run
+                stream.synchronize()
+                barrier()
+                with torch.cuda.stream(stream):
+                    a.record()
+                    for _ in range(warm_runs):
+                        prog.run(sp)
+                    b.record()
+                b.synchronize()
+                ctx.sync()
+                rec["warm_ms"] = allreduce_max(a.elapsed_time(b) / warm_runs)
+                rec["cold_total_ms"] = out[k]["total_ms"] if cycles > 1 else rec["total_ms"]
+                rec["cold_over_warm"] = rec["cold_total_ms"] / rec["warm_ms"]
+                rec["tma_items"] = prog.stats()["tma_items"]
+            out.append(rec)
+    sizes = cyc_obj.sizes
+    cyc_obj.close()
+    ctx.reset(0)
+    return {"steps": out, "states_gb_per_gpu": [x / 1e9 for x in sizes]}
+
+
 # ---------------------------------------------------------------- ours
 def main():
     args = parse()
@@ -575,6 +639,11 @@ def main():
                       "hbm_frac": (sst["hbm_read"] + sst["hbm_write"]) / (sms * 1e-3) / 1e9 / peak}
             del sprog, slay
             ctx.reset(0)
+            # cold vs warm latency, cfg4 and the cfg5 strategy cycle (plan + compile + first run)
+            switch["cold"] = switch_latency(ctx, stream, [W.config4(), W.config4_reverse()], 2,
+                                            allreduce_max, barrier)
+            switch["cfg5_cycle"] = switch_latency(ctx, stream, [W.config5(x) for x in W.CONFIG5_CYCLE], 2,
+                                                  allreduce_max, barrier, warm_runs=5)
 
     cb, cbs = None, None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -8,6 +8,8 @@
 //
 // Not provided: run() and oracle_run(), which execute whole computation
 // graphs (CompGraph / ExecGraph) -- outside the resharding path.
+// DeviceState / SimState (sim.hpp:51-60) are declared as in the reference and
+// drive the SPEC's state-to-state apply_switch.
 #pragma once
 
 #include <set>
@@ -46,6 +48,18 @@ struct TrafficLog {
   int64_t sent_by(DeviceId d) const;
 };
 
+// Per-device simulator state (reference sim.hpp:51-60): tensor id ->
+// (region, payload); regions match placement() of the tensor's current
+// annotation.
+struct DeviceState {
+  std::map<int, std::pair<SliceRegion, Tensor>> store;
+};
+
+struct SimState {
+  std::map<DeviceId, DeviceState> devices;
+  TrafficLog traffic;
+};
+
 // Inverse of placement: concatenate Splits, sum Partials, require Duplicate
 // replicas (and hdim -1 subgroups) to agree within replica_tol.
 // Errors: MissingShard, ShapeMismatch, ReplicaDivergence.
@@ -73,6 +87,12 @@ using ShardKey = std::pair<int, DeviceId>;
 std::map<ShardKey, Tensor> apply_switch(const SwitchPlan& plan,
                                         const std::map<ShardKey, Tensor>& shards,
                                         TrafficLog* traffic = nullptr);
+
+// SPEC.md:428-433 apply_switch(simulator state, plan) -> new state: the
+// moved parameters' source placements (MissingShard if any is absent, e.g. a
+// plan applied twice) are replaced by their destination placements; the
+// plan's traffic is added to state.traffic.  Runs on the GPU as above.
+SimState apply_switch(const SimState& state, const SwitchPlan& plan);
 
 // Traffic a plan implies (what execute_plan / apply_switch log).
 TrafficLog plan_traffic(const CommPlan& plan);

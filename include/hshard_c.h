@@ -174,6 +174,23 @@ enum {
 #define HS_PROG_STREAM_SHARE(sixty_fourths) (((sixty_fourths) & 0xff) << 16)
 int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
                     const size_t* src_off, const size_t* dst_off, int flags, hs_prog** out);
+/* The same over CALLER-OWNED device buffers (the reference's functional
+ * execute_plan takes shards as values, sim.hpp:77-79; a shard is
+ * {device, gpu_ptr, box}): src_ptrs / dst_ptrs[slot * n_virt + v] is the
+ * address of that shard, row-major over its placement box, valid in THIS
+ * process -- any cudaMalloc / framework-allocator pointer on this GPU, or a
+ * peer's buffer mapped with hs_ipc_import (N > 1).  NULL = absent (only the
+ * shards this rank's tasks touch are required).  Buffers are not copied: the
+ * program reshards the framework's tensors in place of a copy through the
+ * arena.  HS_PROG_CE_RELAY is not available in this mode. */
+int hs_prog_compile_ptrs(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
+                         void* const* src_ptrs, void* const* dst_ptrs, int flags, hs_prog** out);
+/* Multi-process buffers: export the allocation holding a local device pointer
+ * (80 bytes: IPC handle, offset, allocation size) for the host to exchange;
+ * import a peer's export into this process (mapped once per allocation,
+ * closed with the context). */
+int hs_ipc_export(hs_ctx* ctx, const void* ptr, unsigned char* out80);
+int hs_ipc_import(hs_ctx* ctx, const unsigned char* in80, void** ptr);
 void hs_prog_destroy(hs_prog* prog);
 /* Run on `stream` (cudaStream_t, NULL = the ctx stream).  Multi-rank programs
  * include device-side barriers; every rank must call run. */

@@ -108,6 +108,27 @@ int hs_prog_compile(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int 
   });
 }
 
+int hs_prog_compile_ptrs(hs_ctx* ctx, const hs_plan* plan, const int* v_to_rank, int n_virt,
+                         void* const* src_ptrs, void* const* dst_ptrs, int flags, hs_prog** out) {
+  return guarded([&] {
+    exec::cuda_check(cudaSetDevice(ctx->c->gpu()), "cudaSetDevice");
+    std::vector<int> map(v_to_rank, v_to_rank + n_virt);
+    auto p = std::make_unique<hs_prog>();
+    p->p = std::make_unique<exec::Program>(*ctx->c, plan->comm ? &*plan->comm : nullptr,
+                                           plan->sw ? &*plan->sw : nullptr, map, nullptr, nullptr, flags,
+                                           src_ptrs, dst_ptrs);
+    *out = p.release();
+  });
+}
+
+int hs_ipc_export(hs_ctx* ctx, const void* ptr, unsigned char* out80) {
+  return guarded([&] { ctx->c->ipc_export(ptr, out80); });
+}
+
+int hs_ipc_import(hs_ctx* ctx, const unsigned char* in80, void** ptr) {
+  return guarded([&] { *ptr = ctx->c->ipc_import(in80); });
+}
+
 void hs_prog_destroy(hs_prog* prog) { delete prog; }
 
 int hs_prog_run(hs_prog* prog, void* stream) {

@@ -1,4 +1,7 @@
 // hshard-b200 C ABI: planner entry points (include/hshard_c.h).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -64,6 +67,7 @@ int hs_plan_switch(int n, const int* tensor_ids, const char* const* src, const c
                    const int64_t* shapes_flat, const int* ndims, int dtype, const char* bw,
                    hs_plan** out) {
   return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
     std::vector<SwitchEntry> diff;
     const int64_t* cursor = shapes_flat;
     for (int i = 0; i < n; ++i) {
@@ -75,6 +79,9 @@ int hs_plan_switch(int n, const int* tensor_ids, const char* const* src, const c
       cursor += ndims[i];
       diff.push_back(std::move(e));
     }
+    if (std::getenv("HS_COMPILE_TRACE"))
+      std::fprintf(stderr, "[plan] parse %zu entries %.2f ms\n", diff.size(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     auto plan = std::make_unique<hs_plan>();
     plan->sw = plan_switch(diff, to_dtype(dtype), parse_bandwidth(bw ? bw : "u"));
     *out = plan.release();
@@ -159,7 +166,7 @@ int hs_align_shard_specs(const char* a, const char* b, char** json) {
 // ---------------------------------------------------------------- strategy source
 namespace {
 
-std::string quoted(const std::string& v) {
+std::string jquote(const std::string& v) {
   std::string o = "\"";
   for (char c : v) {
     if (c == '"' || c == '\\') o += '\\';
@@ -193,16 +200,16 @@ int hs_graph_deduce(const char* graph, char** json) {
     CompGraph g = parse_graph(graph);
     std::string o = "{\"tensors\":[";
     for (const TensorRef& t : g.tensors())
-      o += std::string(t.id ? "," : "") + "{\"id\":" + std::to_string(t.id) + ",\"name\":" + quoted(t.name) +
-           ",\"kind\":" + quoted(op_kind_name(g.node(t.producer).kind)) + ",\"shape\":" +
-           quoted(sym_shape_str(t.shape)) + ",\"dtype\":" + quoted(dtype_name(t.dtype)) +
+      o += std::string(t.id ? "," : "") + "{\"id\":" + std::to_string(t.id) + ",\"name\":" + jquote(t.name) +
+           ",\"kind\":" + jquote(op_kind_name(g.node(t.producer).kind)) + ",\"shape\":" +
+           jquote(sym_shape_str(t.shape)) + ",\"dtype\":" + jquote(dtype_name(t.dtype)) +
            ",\"producer\":" + std::to_string(t.producer) + "}";
     o += "],\"topo\":[";
     const auto order = g.topo_order();
     for (size_t i = 0; i < order.size(); ++i) o += (i ? "," : "") + std::to_string(order[i]);
     o += "],\"symbols\":[";
     const auto syms = g.symbols();
-    for (size_t i = 0; i < syms.size(); ++i) o += (i ? "," : "") + quoted(syms[i]);
+    for (size_t i = 0; i < syms.size(); ++i) o += (i ? "," : "") + jquote(syms[i]);
     o += "],\"strategies\":[";
     for (int s = 0; s < g.strategy_count(); ++s) {
       o += s ? "," : "";
@@ -210,10 +217,10 @@ int hs_graph_deduce(const char* graph, char** json) {
         deduce_graph(g, s);
         o += "{\"ok\":1,\"slots\":[";
         for (const TensorRef& t : g.tensors())
-          o += std::string(t.id ? "," : "") + (t.slots.at(s) ? quoted(t.slots.at(s)->str()) : "null");
+          o += std::string(t.id ? "," : "") + (t.slots.at(s) ? jquote(t.slots.at(s)->str()) : "null");
         o += "]}";
       } catch (const Error& e) {
-        o += "{\"ok\":0,\"error\":" + quoted(errc_name(e.code())) + ",\"message\":" + quoted(e.what()) + "}";
+        o += "{\"ok\":0,\"error\":" + jquote(errc_name(e.code())) + ",\"message\":" + jquote(e.what()) + "}";
       }
     }
     *json = capi::dup_string(o + "]}");
@@ -230,8 +237,8 @@ int hs_graph_diff(const char* graph, int a, int b, const char* bindings, char** 
     for (size_t i = 0; i < diff.size(); ++i) {
       const SwitchEntry& e = diff[i];
       o += std::string(i ? "," : "") + "{\"tensor\":" + std::to_string(e.tensor_id) + ",\"name\":" +
-           quoted(g.tensor(e.tensor_id).name) + ",\"src\":" + quoted(e.src.str()) + ",\"dst\":" +
-           quoted(e.dst.str()) + ",\"shape\":[" + join_ints(e.shape) + "]}";
+           jquote(g.tensor(e.tensor_id).name) + ",\"src\":" + jquote(e.src.str()) + ",\"dst\":" +
+           jquote(e.dst.str()) + ",\"shape\":[" + join_ints(e.shape) + "]}";
     }
     *json = capi::dup_string(o + "]");
   });
@@ -245,7 +252,7 @@ int hs_graph_specialize(const char* graph, int strategy, const char* bindings, c
     std::string o = "{\"phases\":{";
     bool first = true;
     for (const auto& [id, ph] : node_phases(g, strategy)) {
-      o += std::string(first ? "" : ",") + "\"" + std::to_string(id) + "\":" + quoted(exec_phase_name(ph));
+      o += std::string(first ? "" : ",") + "\"" + std::to_string(id) + "\":" + jquote(exec_phase_name(ph));
       first = false;
     }
     o += "},\"exec_graphs\":[";
@@ -255,7 +262,7 @@ int hs_graph_specialize(const char* graph, int strategy, const char* bindings, c
       for (size_t k = 0; k < egs[i].nodes.size(); ++k) {
         const ExecNode& n = egs[i].nodes[k];
         o += std::string(k ? "," : "") + "{\"node\":" + std::to_string(n.node_id) + ",\"comm\":" +
-             (n.is_comm ? "1" : "0") + ",\"phase\":" + quoted(exec_phase_name(n.phase)) +
+             (n.is_comm ? "1" : "0") + ",\"phase\":" + jquote(exec_phase_name(n.phase)) +
              ",\"plan\":" + (n.plan ? dump_plan(*n.plan) : std::string("null")) + "}";
       }
       o += "]}";
@@ -274,7 +281,7 @@ int hs_graph_specialize(const char* graph, int strategy, const char* bindings, c
       }
       o += "]";
     } catch (const Error& e) {
-      o += ",\"pipelines_error\":" + quoted(errc_name(e.code()));
+      o += ",\"pipelines_error\":" + jquote(errc_name(e.code()));
     }
     *json = capi::dup_string(o + "}");
   });

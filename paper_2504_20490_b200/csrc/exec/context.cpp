@@ -61,6 +61,7 @@ Context::~Context() {
   cudaSetDevice(gpu_);
   cudaDeviceSynchronize();
   if (nccl_comm_) nccl::api().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+  for (auto& [key, p] : imported_) cudaIpcCloseMemHandle(p);
   for (int r = 0; r < world_; ++r) {
     if (r == rank_) continue;
     if (peer_arena_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
@@ -149,6 +150,54 @@ void Context::check_barrier_error() {
   int err = 0;
   cuda_check(cudaMemcpy(&err, barrier_error_, sizeof(int), cudaMemcpyDeviceToHost), "barrier err");
   if (err) fail(Errc::DeadlockDetected, "cross-rank barrier timed out (a peer never arrived)");
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no link
+// against libcuda): the base and size of the allocation holding `ptr`.
+namespace {
+using GetRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+GetRangeFn get_range() {
+  static GetRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<GetRangeFn>(f);
+  }();
+  return fn;
+}
+}  // namespace
+
+void Context::ipc_export(const void* ptr, unsigned char out[80]) const {
+  GetRangeFn range = get_range();
+  if (!range) fail(Errc::CudaError, "cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+    fail(Errc::CudaError, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h{};
+  cuda_check(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle(buffer)");
+  const uint64_t off = reinterpret_cast<uint64_t>(ptr) - base, sz = size;
+  std::memcpy(out, &h, 64);
+  std::memcpy(out + 64, &off, 8);
+  std::memcpy(out + 72, &sz, 8);
+}
+
+char* Context::ipc_import(const unsigned char in[80]) {
+  uint64_t off = 0;
+  std::memcpy(&off, in + 64, 8);
+  const std::string key(reinterpret_cast<const char*>(in), 64);
+  auto it = imported_.find(key);
+  if (it == imported_.end()) {
+    cudaIpcMemHandle_t h{};
+    std::memcpy(&h, in, 64);
+    void* p = nullptr;
+    cuda_check(cudaSetDevice(gpu_), "cudaSetDevice");
+    cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(buffer)");
+    it = imported_.emplace(key, static_cast<char*>(p)).first;
+  }
+  return it->second + off;
 }
 
 void Context::clear_error() {

@@ -79,7 +79,7 @@ ShardLoc& Program::loc(int state, int tensor, DeviceId d) {
 
 Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
                  const std::vector<int>& v_to_rank, const size_t* src_off, const size_t* dst_off,
-                 int flags)
+                 int flags, const void* const* src_ptr, const void* const* dst_ptr)
     : ctx_(ctx), flags_(flags), n_virt_(static_cast<int>(v_to_rank.size())), v_to_rank_(v_to_rank) {
   if (!comm == !sw) fail(Errc::UnsupportedOp, "program needs exactly one plan");
   if (!ctx_.peers_open()) fail(Errc::CommError, "open peers before compiling");
@@ -105,7 +105,11 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
   mid_state_ = has_mid ? 1 : -1;
   final_state_ = states_.size() - 1;
 
-  auto add_state = [&](int state, int t, const HetAnnotation& a, const size_t* offs) {
+  const bool ptr_mode = src_ptr || dst_ptr;
+  if (ptr_mode && (flags_ & HS_PROG_CE_RELAY))
+    fail(Errc::UnsupportedOp, "copy-engine relays need arena shards");
+  auto add_state = [&](int state, int t, const HetAnnotation& a, const size_t* offs,
+                       const void* const* ptrs = nullptr) {
     for (const auto& [d, reg] : placements(a, shapes_[t])) {
       if (d < 0 || d >= n_virt_)
         fail(Errc::UnknownDevice, "device " + std::to_string(d) + " has no rank mapping");
@@ -113,6 +117,10 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
       L.region = reg;
       L.rank = v_to_rank_[d];
       L.offset = offs ? offs[static_cast<size_t>(t) * n_virt_ + d] : SIZE_MAX;
+      if (ptrs) {
+        L.ptr = static_cast<char*>(const_cast<void*>(ptrs[static_cast<size_t>(t) * n_virt_ + d]));
+        L.offset = SIZE_MAX;
+      }
       // Every rank's arena has the same size: a caller-supplied offset must
       // leave room for the whole shard (hs_fill_shard / hs_ctx_read check the same).
       if (L.offset != SIZE_MAX) {
@@ -128,20 +136,22 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
     }
   };
   for (int t = 0; t < n_tensors_; ++t) {
-    add_state(0, t, *annos[t].first, src_off);
-    add_state(static_cast<int>(states_.size()) - 1, t, *annos[t].second, dst_off);
+    add_state(0, t, *annos[t].first, ptr_mode ? nullptr : src_off, src_ptr);
+    add_state(static_cast<int>(states_.size()) - 1, t, *annos[t].second, ptr_mode ? nullptr : dst_off, dst_ptr);
   }
   if (has_mid) add_state(1, 0, *comm->mid, nullptr);
   clock_.mark("placements");
 
   for (const auto& [key, L] : states_[0])
-    if (L.rank == ctx_.rank() && L.offset != SIZE_MAX) {
-      host_src_.emplace_back(key.second, key.first, L.offset, L.region.cells() * es_);
+    if (L.rank == ctx_.rank() && present(L)) {
+      host_src_.emplace_back(key.second, key.first, ctx_.is_analysis() ? nullptr : addr_of(L),
+                             L.region.cells() * es_);
       stats_.src_bytes += L.region.cells() * es_;
     }
   for (const auto& [key, L] : states_.back())
-    if (L.rank == ctx_.rank() && L.offset != SIZE_MAX) {
-      host_dst_.emplace_back(key.second, key.first, L.offset, L.region.cells() * es_);
+    if (L.rank == ctx_.rank() && present(L)) {
+      host_dst_.emplace_back(key.second, key.first, ctx_.is_analysis() ? nullptr : addr_of(L),
+                             L.region.cells() * es_);
       stats_.dst_bytes += L.region.cells() * es_;
     }
   lower(comm, sw);
@@ -517,10 +527,10 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   clock_.mark("accounting");
   for (const BoxTask& t : mine) {
     for (const Operand& o : t.dsts)
-      if (loc(o.state, t.tensor, o.dev).offset == SIZE_MAX)
+      if (!present(loc(o.state, t.tensor, o.dev)))
         fail(Errc::MissingShard, "destination shard of device " + std::to_string(o.dev) + " has no buffer");
     for (const Operand& o : t.terms)
-      if (loc(o.state, t.tensor, o.dev).offset == SIZE_MAX)
+      if (!present(loc(o.state, t.tensor, o.dev)))
         fail(Errc::MissingShard, "source shard of device " + std::to_string(o.dev) + " has no buffer");
   }
   build_tables(mine);
@@ -1327,12 +1337,14 @@ Program::Flat Program::flatten(const BoxTask& bt) {
     f.ext.push_back(1);
     for (auto& s : f.st) s.push_back(1);
   }
-  // Alignment from arena offsets: every rank's arena base is 256-byte aligned.
+  // Alignment from arena offsets (every rank's arena base is 256-byte
+  // aligned) or from the caller's buffer addresses.
   const int rd = static_cast<int>(f.ext.size());
   auto ok = [&](int v) {
     if ((f.ext.back() * es_) % v) return false;
     for (size_t k = 0; k < f.locs.size(); ++k) {
-      if ((f.locs[k]->offset + f.elem_off[k] * es_) % v) return false;
+      const uint64_t a = f.locs[k]->ptr ? reinterpret_cast<uintptr_t>(f.locs[k]->ptr) : f.locs[k]->offset;
+      if ((a + f.elem_off[k] * es_) % v) return false;
       for (int j = 0; j + 1 < rd; ++j)
         if ((f.st[k][j] * es_) % v) return false;
     }
@@ -1397,7 +1409,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     for (size_t g = 0; g < bt.groups.size(); ++g) td.gsize[g] = static_cast<uint8_t>(bt.groups[g]);
     for (size_t k = 0; k < f.locs.size(); ++k) {
       TermDesc tm{};
-      tm.base = ctx_.arena_of(f.locs[k]->rank) + f.locs[k]->offset + f.elem_off[k] * es_;
+      tm.base = addr_of(*f.locs[k]) + f.elem_off[k] * es_;
       for (int j = 1; j < 4; ++j) tm.stride[j - 1] = j < rd ? f.st[k][rd - 1 - j] : 0;
       H.terms.push_back(tm);
     }
@@ -1775,7 +1787,7 @@ void Program::run_host_async(const void* const* src_host, void* const* dst_host,
   cuda_check(cudaStreamWaitEvent(h2d, host_ev_[1], 0), "stream wait");
   for (const auto& [d, t, off, bytes] : host_src_) {
     const void* h = src_host[static_cast<size_t>(t) * n_virt_ + d];
-    if (h) cuda_check(cudaMemcpyAsync(ctx_.arena() + off, h, bytes, cudaMemcpyHostToDevice, h2d), "H2D");
+    if (h) cuda_check(cudaMemcpyAsync(off, h, bytes, cudaMemcpyHostToDevice, h2d), "H2D");
   }
   cuda_check(cudaEventRecord(host_ev_[0], h2d), "event record");
   cuda_check(cudaStreamWaitEvent(compute, host_ev_[0], 0), "stream wait");
@@ -1790,7 +1802,7 @@ void Program::run_host_async(const void* const* src_host, void* const* dst_host,
   cuda_check(cudaStreamWaitEvent(d2h, host_ev_[1], 0), "stream wait");
   for (const auto& [d, t, off, bytes] : host_dst_) {
     void* h = dst_host[static_cast<size_t>(t) * n_virt_ + d];
-    if (h) cuda_check(cudaMemcpyAsync(h, ctx_.arena() + off, bytes, cudaMemcpyDeviceToHost, d2h), "D2H");
+    if (h) cuda_check(cudaMemcpyAsync(h, off, bytes, cudaMemcpyDeviceToHost, d2h), "D2H");
   }
   cuda_check(cudaEventRecord(host_ev_[2], d2h), "event record");
 }
@@ -1799,7 +1811,7 @@ void Program::run_host(const void* const* src_host, void* const* dst_host) {
   cudaStream_t s = ctx_.stream();
   for (const auto& [d, t, off, bytes] : host_src_) {
     const void* h = src_host[static_cast<size_t>(t) * n_virt_ + d];
-    if (h) cuda_check(cudaMemcpyAsync(ctx_.arena() + off, h, bytes, cudaMemcpyHostToDevice, s), "H2D");
+    if (h) cuda_check(cudaMemcpyAsync(off, h, bytes, cudaMemcpyHostToDevice, s), "H2D");
   }
   run(s);
   // Peers read this rank's sources over NVLink during their run: the next
@@ -1808,7 +1820,7 @@ void Program::run_host(const void* const* src_host, void* const* dst_host) {
   if (ctx_.world() > 1 && !nccl_mode_ && !remote_final_writes_) ctx_.barrier(s);
   for (const auto& [d, t, off, bytes] : host_dst_) {
     void* h = dst_host[static_cast<size_t>(t) * n_virt_ + d];
-    if (h) cuda_check(cudaMemcpyAsync(h, ctx_.arena() + off, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    if (h) cuda_check(cudaMemcpyAsync(h, off, bytes, cudaMemcpyDeviceToHost, s), "D2H");
   }
   cuda_check(cudaStreamSynchronize(s), "run_host sync");
   ctx_.check_barrier_error();

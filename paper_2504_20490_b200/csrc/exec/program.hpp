@@ -76,6 +76,12 @@ class Context {
   unsigned long long* scratch_counter() const { return counter_; }
   int* error_flag() const { return barrier_error_; }
 
+  // Caller-owned buffers across processes: export the allocation holding a
+  // local device pointer (IPC handle + offset), import a peer's export
+  // (mapped once per allocation; closed with the context).
+  void ipc_export(const void* ptr, unsigned char out[80]) const;
+  char* ipc_import(const unsigned char in[80]);
+
   // NCCL communicator over the same ranks (HS_PROG_NCCL baseline transport).
   void nccl_init(const unsigned char id[128]);
   void* nccl_comm() const { return nccl_comm_; }
@@ -92,6 +98,7 @@ class Context {
   unsigned int** d_peer_flags_ = nullptr;
   std::vector<char*> peer_arena_;
   std::vector<unsigned int*> peer_flags_;
+  std::map<std::string, char*> imported_;  // IPC handle bytes -> mapped base
   unsigned int epoch_ = 0;
   bool peers_open_ = false;
   cudaStream_t stream_ = nullptr;
@@ -106,6 +113,7 @@ struct ShardLoc {
   SliceRegion region;
   int rank = -1;
   size_t offset = SIZE_MAX;  // arena byte offset on `rank`
+  char* ptr = nullptr;       // caller-owned buffer (hs_prog_compile_ptrs): address in this process
   int subgroup = 0;          // annotation subgroup of the device
   int eff_hdim = -1;         // effective hdim of the annotation
 };
@@ -166,8 +174,13 @@ struct ProgramStats {
 class Program {
  public:
   // Plan kinds: a CommPlan (one tensor) or a fused switch plan (many tensors).
+  // Shards live in the arenas (src_off / dst_off: per (tensor slot, virtual
+  // device) arena offsets on the owning rank) or in caller-owned buffers
+  // (src_ptr / dst_ptr: addresses valid in THIS process -- local allocations,
+  // or peers' buffers mapped with hs_ipc_import; null = absent).
   Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw, const std::vector<int>& v_to_rank,
-          const size_t* src_off, const size_t* dst_off, int flags);
+          const size_t* src_off, const size_t* dst_off, int flags, const void* const* src_ptr = nullptr,
+          const void* const* dst_ptr = nullptr);
   ~Program();
 
   void run(cudaStream_t s);
@@ -221,6 +234,8 @@ class Program {
   bool tma_capable(const BoxTask& bt);
   void build_tables(const std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);
+  char* addr_of(const ShardLoc& L) const { return L.ptr ? L.ptr : ctx_.arena_of(L.rank) + L.offset; }
+  static bool present(const ShardLoc& L) { return L.ptr || L.offset != SIZE_MAX; }
 
   Context& ctx_;
   int flags_ = 0;
@@ -279,8 +294,8 @@ class Program {
   ProgramStats stats_;
   StageClock clock_;
   std::vector<BoxTask> analysed_;  // analysis contexts: this rank's final tasks
-  // host-buffer path: (virtual device, tensor) -> (offset, bytes) on this rank
-  std::vector<std::tuple<DeviceId, int, size_t, size_t>> host_src_, host_dst_;
+  // host-buffer path: (virtual device, tensor) -> (device address, bytes) on this rank
+  std::vector<std::tuple<DeviceId, int, char*, size_t>> host_src_, host_dst_;
 };
 
 }  // namespace hshard::exec

@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes
 import json
 import os
+import time
 from ctypes import c_int, c_size_t, c_ulonglong, c_void_p
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -250,6 +251,234 @@ class ShardLayout:
             self.ctx.write_array(rec["offset"], np.full(rec["bytes"], 0xA5, dtype=np.uint8))
 
 
+class PointerLayout:
+    """Caller-owned shard buffers (hs_prog_compile_ptrs): {(slot, dev): device address}
+    valid in this process -- e.g. torch tensors' data_ptr() on this GPU, or peers'
+    buffers mapped by exchange_pointers().  Each buffer is row-major over the shard's
+    placement box in the plan's dtype; the program reads / writes them in place."""
+
+    def __init__(self, n_virtual: int, n_slots: int, src: Dict[Tuple[int, int], int],
+                 dst: Dict[Tuple[int, int], int], v_to_rank: Sequence[int]):
+        self.n_virtual, self.v_to_rank = n_virtual, list(v_to_rank)
+        self.entries = [None] * n_slots
+        n = max(1, n_slots * n_virtual)
+        self.src_ptr, self.dst_ptr = (c_void_p * n)(), (c_void_p * n)()
+        for (slot, dev), ptr in src.items():
+            self.src_ptr[slot * n_virtual + dev] = ptr
+        for (slot, dev), ptr in dst.items():
+            self.dst_ptr[slot * n_virtual + dev] = ptr
+
+
+def exchange_pointers(ctx: Context, local: Dict[Tuple[str, int, int], int], group=None) -> Dict:
+    """N > 1: every rank passes its OWN shards' device pointers {(side, slot, dev): ptr};
+    returns every rank's shards mapped into this process (hs_ipc_export on the owner,
+    an all-gather of the 80-byte exports, hs_ipc_import here)."""
+    import torch.distributed as dist
+    mine = []
+    for key, ptr in sorted(local.items()):
+        buf = ctypes.create_string_buffer(80)
+        check(LIB.hs_ipc_export(ctx.handle, c_void_p(ptr), buf))
+        mine.append((key, buf.raw))
+    allv = [None] * ctx.world
+    dist.all_gather_object(allv, mine, group=group)
+    out = dict(local)
+    for r, items in enumerate(allv):
+        if r == ctx.rank:
+            continue
+        for key, blob in items:
+            p = c_void_p()
+            check(LIB.hs_ipc_import(ctx.handle, blob, ctypes.byref(p)))
+            out[key] = p.value
+    return out
+
+
+class StateLayout:
+    """One layout state of a set of tensors -- e.g. every parameter of a model under one
+    parallel strategy -- packed symmetrically into the arenas (the same per-rank dense
+    packing as ShardLayout, for one side).  Graph switches chain states: the destination
+    state of S1->S2 is the source state of S2->S3 (SPEC.md:428-433 apply_switch, where a
+    switch releases the old shards), so a cycle needs only two states resident at a time.
+
+    entries: [(slot, tensor_id, annotation, shape)].  `base`: arena offset to place the
+    state at (None = bump-allocate); StateLayout.bytes_needed() sizes it first.
+    """
+
+    def __init__(self, ctx: Context, entries, dtype: str, n_virtual: int,
+                 v_to_rank: Optional[Sequence[int]] = None, base: Optional[int] = None):
+        self.ctx, self.dtype, self.n_virtual = ctx, dtype, n_virtual
+        self.v_to_rank = list(v_to_rank) if v_to_rank is not None else block_map(n_virtual, ctx.world)
+        self.es = H.DTYPE_BYTES[dtype]
+        self.entries = [(int(slot), int(tid), anno, [int(x) for x in shape]) for slot, tid, anno, shape in entries]
+        self.n_slots = max((e[0] for e in self.entries), default=-1) + 1
+        self.recs, used = self._pack(self.entries, self.es, self.n_virtual, self.v_to_rank, ctx.world)
+        self.size = max(used) + 256
+        self.base = ctx.alloc(self.size) if base is None else int(base)
+        if self.base + self.size > ctx.arena_bytes:
+            raise H.HshardError("ShapeMismatch", "state does not fit the arena")
+        for rec in self.recs.values():
+            rec["offset"] = self.base + rec["rel"]
+
+    @staticmethod
+    def _pack(entries, es, n_virtual, v_to_rank, world):
+        used = [0] * world
+        recs = {}
+        for slot, tid, anno, shape in entries:
+            devs = sorted({x for g in H.parse_annotation(anno)["groups"] for x in g})
+            for dev in devs:
+                if dev >= n_virtual:
+                    raise H.HshardError("UnknownDevice", f"device {dev} >= n_virtual")
+                p = _box(anno, shape, dev)
+                ext = [hi - lo for lo, hi in p["bounds"]]
+                nbytes = int(np.prod(ext)) * es if ext else es
+                r = v_to_rank[dev]
+                off = (used[r] + 255) // 256 * 256
+                used[r] = off + nbytes
+                recs[(slot, dev)] = {"slot": slot, "dev": dev, "rank": r, "rel": off, "bytes": nbytes, "ext": ext,
+                                     "bounds": p["bounds"], "partial": p["partial"], "anno": anno,
+                                     "shape": shape, "tid": tid}
+        return recs, used
+
+    @staticmethod
+    def bytes_needed(entries, dtype: str, n_virtual: int, world: int, v_to_rank=None) -> int:
+        m = list(v_to_rank) if v_to_rank is not None else block_map(n_virtual, world)
+        _, used = StateLayout._pack([(s, t, a, [int(x) for x in sh]) for s, t, a, sh in entries],
+                                    H.DTYPE_BYTES[dtype], n_virtual, m, world)
+        return max(used) + 256
+
+    def offsets(self, tensor_ids: Sequence[int]):
+        """Offset table for a plan whose tensor slots are `tensor_ids` (slot i = the plan's
+        i-th tensor): arr[i * n_virtual + dev]; tensors this state lacks stay absent."""
+        by_tid = {}
+        for (slot, dev), rec in self.recs.items():
+            by_tid.setdefault(rec["tid"], {})[dev] = rec["offset"]
+        n = len(tensor_ids) * self.n_virtual
+        arr = (c_size_t * max(1, n))(*([SIZE_MAX] * max(1, n)))
+        for i, tid in enumerate(tensor_ids):
+            for dev, off in by_tid.get(int(tid), {}).items():
+                arr[i * self.n_virtual + dev] = off
+        return arr
+
+    def local(self):
+        return {k: v for k, v in self.recs.items() if v["rank"] == self.ctx.rank}
+
+    def fill(self, seed: int, mode: str = "grid", stream=None) -> None:
+        m = 0 if mode == "grid" else 1
+        for (slot, dev), rec in self.local().items():
+            arr, n = _shape_arr(rec["shape"])
+            check(LIB.hs_fill_shard(self.ctx.handle, rec["anno"].encode(), arr, n, H.DTYPES[self.dtype], dev,
+                                    rec["offset"], seed, rec["tid"], m, stream))
+
+    def verify(self, seed: int) -> int:
+        """Cells of this rank's shards that differ from the logical grid tensors."""
+        bad = 0
+        for (slot, dev), rec in self.local().items():
+            arr, n = _shape_arr(rec["shape"])
+            out = c_ulonglong()
+            check(LIB.hs_verify_shard(self.ctx.handle, rec["anno"].encode(), arr, n, H.DTYPES[self.dtype], dev,
+                                      rec["offset"], seed, rec["tid"], ctypes.byref(out), None))
+            bad += out.value
+        return bad
+
+
+class Transition:
+    """A (source state, destination state) pair in the form Program compiles against:
+    offset tables indexed by the plan's tensor slots (a switch plan lists only the
+    parameters that move, in its own order; shards are matched by tensor id)."""
+
+    def __init__(self, plan: "H.Plan", src: StateLayout, dst: StateLayout):
+        if src.n_virtual != dst.n_virtual or src.v_to_rank != dst.v_to_rank:
+            raise H.HshardError("UnknownDevice", "states map virtual devices differently")
+        self.src_state, self.dst_state = src, dst
+        self.n_virtual, self.v_to_rank = src.n_virtual, src.v_to_rank
+        if plan.kind == "comm":
+            tids = [0]
+        else:
+            tids = [int(e[0]) for e in plan.meta["entries"]]
+        self.entries = [(t, None, None, None) for t in tids]
+        self.src_off, self.dst_off = src.offsets(tids), dst.offsets(tids)
+
+
+class SwitchCache:
+    """Plans and compiled programs cached per (source, destination) strategy
+    (host planning is the same order as a switch's
+    execution, so a strategy cycle must not re-plan).  Keys: the switch's
+    parameter moves + dtype (plan), and the plan with the two states' placement
+    + program flags (program)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self.plans: Dict[tuple, "H.Plan"] = {}
+        self.programs: Dict[tuple, "Program"] = {}
+
+    def plan(self, entries, dtype: str):
+        key = (tuple((int(t), s, d, tuple(int(x) for x in sh)) for t, s, d, sh in entries), dtype)
+        p = self.plans.get(key)
+        hit = p is not None
+        if not hit:
+            p = self.plans[key] = H.plan_switch(entries, dtype)
+        return p, hit
+
+    def program(self, plan, src: StateLayout, dst: StateLayout, flags: int = 0):
+        key = (id(plan), src.base, src.size, dst.base, dst.size, flags)
+        prog = self.programs.get(key)
+        hit = prog is not None
+        if not hit:
+            prog = self.programs[key] = Program(self.ctx, plan, Transition(plan, src, dst), flags)
+        return prog, hit
+
+    def close(self):
+        for p in self.programs.values():
+            p.close()
+        self.programs.clear()
+        self.plans.clear()
+
+
+class StrategyCycle:
+    """Graph switching through a cycle of parallel strategies:
+    one StateLayout per strategy, alternating between the low and the high end of
+    the arena (a switch releases the old state, so two states are
+    resident at a time), and a SwitchCache so that the second time round no plan is
+    re-planned and no program recompiled.
+
+    steps: list of switch transition lists [(tensor_id, src, dst, shape)], where
+    step k's destinations are step k+1's sources; when the last step returns to the
+    first strategy the cycle reuses the first state's placement."""
+
+    def __init__(self, ctx: Context, steps, dtype: str, n_virtual: int, flags: int = 0):
+        self.ctx, self.steps, self.dtype, self.n_virtual, self.flags = ctx, steps, dtype, n_virtual, flags
+        ents = [[(i, tid, s, shp) for i, (tid, s, d, shp) in enumerate(st)] for st in steps]
+        ents.append([(i, tid, d, shp) for i, (tid, s, d, shp) in enumerate(steps[-1])])
+        closed = [e[1:] for e in ents[-1]] == [e[1:] for e in ents[0]]
+        self.sizes = [StateLayout.bytes_needed(e, dtype, n_virtual, ctx.world) for e in ents]
+        top = ctx.arena_bytes // 256 * 256
+        need = max(self.sizes[k] + self.sizes[k + 1] for k in range(len(steps)))
+        if need > top:
+            raise H.HshardError("ShapeMismatch", f"two states need {need} bytes per GPU, arena {top}")
+        if closed and len(steps) % 2 == 1:
+            raise H.HshardError("UnsupportedOp", "a closed cycle needs an even number of steps")
+        self.states: List[StateLayout] = []
+        for k, e in enumerate(ents):
+            if k == len(ents) - 1 and closed:
+                self.states.append(self.states[0])
+                continue
+            base = 0 if k % 2 == 0 else (top - self.sizes[k]) // 256 * 256
+            self.states.append(StateLayout(ctx, e, dtype, n_virtual, base=base))
+        self.cache = SwitchCache(ctx)
+
+    def prepare(self, k: int):
+        """Plan (cached) and compile (cached) step k -> (program, info)."""
+        t0 = time.perf_counter()
+        plan, plan_hit = self.cache.plan(self.steps[k], self.dtype)
+        t1 = time.perf_counter()
+        prog, prog_hit = self.cache.program(plan, self.states[k], self.states[k + 1], self.flags)
+        t2 = time.perf_counter()
+        return prog, {"plan_cached": plan_hit, "program_cached": prog_hit, "plan_ms": (t1 - t0) * 1e3,
+                      "compile_ms": (t2 - t1) * 1e3}
+
+    def close(self):
+        self.cache.close()
+
+
 def _shape_arr(shape):
     return i64_array(shape), len(shape)
 
@@ -257,12 +486,16 @@ def _shape_arr(shape):
 class Program:
     """hs_prog: a plan compiled for this rank."""
 
-    def __init__(self, ctx: Context, plan: H.Plan, layout: ShardLayout, flags: int = 0):
+    def __init__(self, ctx: Context, plan: H.Plan, layout, flags: int = 0):
         self.ctx, self.plan, self.layout, self.flags = ctx, plan, layout, flags
         m = (c_int * layout.n_virtual)(*layout.v_to_rank)
         h = c_void_p()
-        check(LIB.hs_prog_compile(ctx.handle, plan.handle, m, layout.n_virtual, layout.src_off,
-                                  layout.dst_off, flags, ctypes.byref(h)))
+        if isinstance(layout, PointerLayout):
+            check(LIB.hs_prog_compile_ptrs(ctx.handle, plan.handle, m, layout.n_virtual, layout.src_ptr,
+                                           layout.dst_ptr, flags, ctypes.byref(h)))
+        else:
+            check(LIB.hs_prog_compile(ctx.handle, plan.handle, m, layout.n_virtual, layout.src_off,
+                                      layout.dst_off, flags, ctypes.byref(h)))
         self._h = h
 
     def run(self, stream=None) -> None:

@@ -148,6 +148,12 @@ def config4() -> Workload:
     return switch_workload("cfg4", ps, tp_pp(2, 4, 32), tp_pp(4, 2, 32), 8)
 
 
+def config4_reverse() -> Workload:
+    """The switch back, TP4xPP2 -> TP2xPP4 (with config4, a two-step strategy cycle)."""
+    ps = llama_params(32, 4096, 11008, 32000)
+    return switch_workload("cfg4_rev", ps, tp_pp(4, 2, 32), tp_pp(2, 4, 32), 8)
+
+
 LLAMA13B = dict(layers=40, hidden=5120, ffn=13824, vocab=32000)
 
 

@@ -159,6 +159,31 @@ static void gpu_tests() {
     missing = e.code() == Errc::MissingShard;
   }
   CHECK(missing);
+  // the SPEC's state-to-state form over the reference's SimState / DeviceState
+  SimState sim;
+  for (const auto& e : diff)
+    for (auto& [d, t] : scatter(e.src, iota(e.shape, DType::BF16, e.tensor_id)))
+      sim.devices[d].store[e.tensor_id] = {placement(e.src, e.shape, d), t};
+  const SimState moved_sim = apply_switch(sim, plan_switch(diff, DType::BF16));
+  CHECK(moved_sim.traffic.total() > 0);
+  for (const auto& e : diff) {
+    std::map<DeviceId, Tensor> shards;
+    for (const auto& [d, ds] : moved_sim.devices)
+      if (ds.store.count(e.tensor_id)) shards[d] = ds.store.at(e.tensor_id).second;
+    CHECK(reassemble(e.dst, shards, e.shape).bit_equal(iota(e.shape, DType::BF16, e.tensor_id)));
+  }
+  const SimState back_sim = apply_switch(moved_sim, plan_switch(back, DType::BF16));
+  for (const auto& [d, ds] : sim.devices)
+    for (const auto& [tid, rt] : ds.store) CHECK(back_sim.devices.at(d).store.at(tid).second.bit_equal(rt.second));
+  bool twice = false;
+  try {
+    apply_switch(moved_sim, plan_switch(diff, DType::BF16));
+  } catch (const Error& e) {
+    twice = e.code() == Errc::MissingShard;
+  }
+  CHECK(twice);
+  // repeated execute_plan of one plan reuses its cached context and program
+  for (int r = 0; r < 3; ++r) CHECK(reassemble(dst, execute_plan(plan, scatter(src, x)), shape).bit_equal(x));
 }
 
 int main(int argc, char** argv) {

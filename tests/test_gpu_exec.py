@@ -378,3 +378,67 @@ def test_switch_round_trip_random_strategies(gpu_ctx):
         if done == 20:
             break
     assert done == 20
+
+
+def test_strategy_cycle_cached_round_trip(gpu_ctx):
+    """A Llama-shaped 4-strategy cycle (cfg5's S1->S2->S3->S4->S1, shapes / 32)
+    through chained layout states twice: the second cycle re-plans and
+    recompiles nothing (SwitchCache hits), every state equals the logical
+    tensors, and the round trip returns S1 bit-exactly."""
+    from paper_2504_20490_b200.executor import StrategyCycle
+    steps = []
+    for x in W.CONFIG5_CYCLE:
+        steps.append([(tid, s, d, tuple(max(8, v // 32) for v in shp)) for tid, s, d, shp in W.config5(x).transitions])
+    mark = gpu_ctx.alloc(0)
+    cyc = StrategyCycle(gpu_ctx, steps, "bf16", 8)
+    try:
+        assert cyc.states[-1] is cyc.states[0]
+        cyc.states[0].fill(7)
+        gpu_ctx.sync()
+        for rnd in range(2):
+            for k in range(len(steps)):
+                prog, info = cyc.prepare(k)
+                assert info["plan_cached"] == (rnd == 1) and info["program_cached"] == (rnd == 1)
+                prog.run()
+                gpu_ctx.sync()
+                assert cyc.states[k + 1].verify(7) == 0, (rnd, k)
+    finally:
+        cyc.close()
+        gpu_ctx.reset(mark)
+
+
+@pytest.mark.parametrize("name", ["cfg2e", "cfg3b", "cfg1C"])
+def test_caller_owned_torch_buffers(gpu_ctx, name):
+    """hs_prog_compile_ptrs: the program reshards framework-allocated tensors
+    (torch.empty on cuda:0, caching-allocator sub-allocations) in place -- no
+    arena -- bit-exact against the oracle (shards are
+    {device, gpu_ptr, box}; reference sim.hpp:77-79)."""
+    import torch
+    from paper_2504_20490_b200.executor import PointerLayout, Program
+    w = W.by_name(name)
+    tid, src, dst, shape = w.transitions[0]
+    shape = [s // 16 for s in shape]
+    plan = H.classify(src, dst, shape, w.dtype)
+    ref_src = ox.scatter(src, shape, w.dtype, 8, 0, "real")
+    want = ox.execute_plan(plan.json(), ref_src, w.dtype)
+    tdt = {"bf16": torch.int16, "f32": torch.float32}[w.dtype]
+    keep, sp, dp = [], {}, {}
+    for dev, a in ref_src.items():
+        t = torch.from_numpy(a.view(np.int16) if w.dtype == "bf16" else a).to("cuda:0")
+        keep.append(t)
+        sp[(0, dev)] = t.data_ptr()
+    outs = {}
+    for dev, a in want.items():
+        t = torch.full(a.shape, 7, dtype=tdt, device="cuda:0")
+        keep.append(t)
+        outs[dev] = t
+        dp[(0, dev)] = t.data_ptr()
+    lay = PointerLayout(w.n_virtual, 1, sp, dp, [0] * w.n_virtual)
+    for flags in (0, 2 | 4 | 8):
+        prog = Program(gpu_ctx, plan, lay, flags)
+        prog.run(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        for dev, a in want.items():
+            got = outs[dev].cpu().numpy()
+            assert np.array_equal(got.view(np.uint8), a.view(np.uint8)), (name, flags, dev)
+        prog.close()
