@@ -510,28 +510,41 @@ def main():
     total_dst = sum(r["bytes"] for r in lay.dst.values())
     value = total_dst / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (phase) on this rank
+    # roofline of the dominant kernel: the (rank, launched phase) with the longest
+    # event-timed duration, max over ranks; its algorithmic bytes per launch come from
+    # that rank's compiled-program accounting.  Bound = whichever of HBM (local reads +
+    # writes vs the measured HBM peak) and NVLink (peer reads + peer stores vs the
+    # measured per-direction peer-copy rate) that kernel runs closer to.
     peak, peak_kind = measured_peaks()
-    dom = max(range(len(phase_ms)), key=lambda p: phase_ms[p])
-    rd, wr, nvin = st["phase_bytes"][dom]
-    kern_s = phase_ms[dom] * 1e-3
-    if world == 1 or nvin == 0:
-        achieved = (rd + wr) / kern_s / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(w.name, dom),
-                "kernel": (f"{('box_phase_tma_static_kernel' if world == 1 else 'box_phase_tma_tail_kernel' if not st.get('streamed') else 'box_phase_tma_kernel') if st['tma_items'] else 'box_phase_kernel'} "
-                           f"phase {dom} of {st['phases']} (plan phases {st['plan_phases']}, "
-                           f"fused tasks {st['fused_tasks']})"),
-                "bytes_per_launch": rd + wr, "launch_ms": phase_ms[dom],
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "share_of_step": phase_ms[dom] / ms if ms else None}
+    mine_k = {"rank": rank, "phase_ms": phase_ms, "phase_bytes": st["phase_bytes"],
+              "phase_kernels": st["phase_kernels"], "streamed": st["streamed"]}
+    ranks_k = [mine_k]
+    if world > 1:
+        import torch.distributed as dist
+        ranks_k = [None] * world
+        dist.all_gather_object(ranks_k, mine_k)
+    crit = max(ranks_k, key=lambda r_: max(r_["phase_ms"]))
+    dom = max(range(len(crit["phase_ms"])), key=lambda p: crit["phase_ms"][p])
+    rd, wr, nvb = crit["phase_bytes"][dom]
+    kern_s = crit["phase_ms"][dom] * 1e-3
+    hbm_ach, nv_ach = (rd + wr) / kern_s / 1e9, nvb / kern_s / 1e9
+    kname = "+".join(crit["phase_kernels"][dom])
+    common = {"kernel": (f"{kname} (rank {crit['rank']}, launched phase {dom} of {len(crit['phase_ms'])}, "
+                         f"plan phases {st['plan_phases']}, fused tasks {st['fused_tasks']})"),
+              "launch_ms": crit["phase_ms"][dom], "critical_rank": crit["rank"],
+              "share_of_step": crit["phase_ms"][dom] / ms if ms else None,
+              "per_rank_launch_ms": [max(r_["phase_ms"]) for r_ in ranks_k]}
+    if world == 1 or hbm_ach / peak >= nv_ach / NVLINK_GBS:
+        roof = {"bound": "hbm", "achieved": hbm_ach, "peak": peak, "unit": "GB/s", "frac": hbm_ach / peak,
+                "traffic": ncu_traffic(w.name if world == 1 else f"{w.name}@n{world}", dom),
+                "bytes_per_launch": rd + wr, "nvlink_achieved": nv_ach,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", **common}
     else:
-        achieved = nvin / kern_s / 1e9
-        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_GBS, "unit": "GB/s",
-                "frac": achieved / NVLINK_GBS, "traffic": None,
-                "kernel": f"box_phase_kernel phase {dom}", "bytes_per_launch": nvin,
-                "launch_ms": phase_ms[dom], "hbm_achieved": (rd + wr) / kern_s / 1e9,
-                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)"}
+        roof = {"bound": "nvlink", "achieved": nv_ach, "peak": NVLINK_GBS, "unit": "GB/s",
+                "frac": nv_ach / NVLINK_GBS, "traffic": ncu_traffic(f"{w.name}@n{world}", dom),
+                "bytes_per_launch": nvb, "hbm_achieved": hbm_ach, "hbm_bytes_per_launch": rd + wr,
+                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md; 900 nominal)",
+                **common}
 
     # ---- NCCL-convention bus GB/s, and the step
     # floor = max over GPUs of max(NVLink bytes / link peak, HBM bytes / HBM

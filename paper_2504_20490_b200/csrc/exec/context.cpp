@@ -5,7 +5,9 @@
 // (rank, offset) pair names a buffer on any GPU.  Peers' arenas are mapped
 // once through CUDA IPC (cudaIpcOpenMemHandle with lazy peer access), after
 // which a kernel on this GPU can load any peer's shard directly over NVLink.
+#include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <string>
 
 #include "nccl_dyn.hpp"
@@ -38,7 +40,58 @@ Context::Context(int rank, int world, int gpu, size_t arena_bytes)
   cuda_check(cudaMemcpy(d_peer_flags_, peer_flags_.data(), world * sizeof(unsigned int*),
                         cudaMemcpyHostToDevice),
              "cudaMemcpy(peers)");
+  const char* pool_mb = std::getenv("HS_TABLE_POOL_MB");
+  pool_bytes_ = static_cast<size_t>(pool_mb ? std::atoll(pool_mb) : 1024) << 20;
+  if (pool_bytes_ && cudaMalloc(&pool_, pool_bytes_) == cudaSuccess) {
+    pool_free_[0] = pool_bytes_;
+  } else {
+    cudaGetLastError();  // no pool: every table block is a cudaMalloc
+    pool_ = nullptr;
+    pool_bytes_ = 0;
+  }
   cuda_check(cudaDeviceSynchronize(), "context init");
+}
+
+void* Context::table_alloc(size_t bytes) {
+  bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t{255};
+  for (auto it = pool_free_.begin(); it != pool_free_.end(); ++it)
+    if (it->second >= bytes) {
+      const size_t off = it->first, left = it->second - bytes;
+      pool_free_.erase(it);
+      if (left) pool_free_[off + bytes] = left;
+      pool_used_[off] = bytes;
+      return pool_ + off;
+    }
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(tables)");
+  return p;
+}
+
+void Context::table_free(void* p) {
+  char* c = static_cast<char*>(p);
+  if (!pool_ || c < pool_ || c >= pool_ + pool_bytes_) {
+    cudaFree(p);
+    return;
+  }
+  const size_t off = static_cast<size_t>(c - pool_);
+  auto u = pool_used_.find(off);
+  if (u == pool_used_.end()) return;
+  size_t start = off, len = u->second;
+  pool_used_.erase(u);
+  auto next = pool_free_.lower_bound(start);
+  if (next != pool_free_.end() && next->first == start + len) {
+    len += next->second;
+    next = pool_free_.erase(next);
+  }
+  if (next != pool_free_.begin()) {
+    auto prev = std::prev(next);
+    if (prev->first + prev->second == start) {
+      start = prev->first;
+      len += prev->second;
+      pool_free_.erase(prev);
+    }
+  }
+  pool_free_[start] = len;
 }
 
 Context::Context(AnalysisTag, int rank, int world) : rank_(rank), world_(world), gpu_(-1) {
@@ -67,6 +120,7 @@ Context::~Context() {
     if (peer_arena_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
     if (peer_flags_[r]) cudaIpcCloseMemHandle(peer_flags_[r]);
   }
+  if (pool_) cudaFree(pool_);
   cudaFree(d_peer_flags_);
   cudaFree(counter_);
   cudaFree(barrier_error_);

@@ -29,6 +29,7 @@
 #include <set>
 #include <sstream>
 #include <tuple>
+#include <unordered_map>
 
 #include "hshard_c.h"
 #include "nccl_dyn.hpp"
@@ -108,9 +109,20 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
   const bool ptr_mode = src_ptr || dst_ptr;
   if (ptr_mode && (flags_ & HS_PROG_CE_RELAY))
     fail(Errc::UnsupportedOp, "copy-engine relays need arena shards");
+  // placements per distinct (annotation, shape): a model's parameters repeat a
+  // few layouts, and placements() validates the annotation each time
+  std::unordered_map<std::string, std::map<DeviceId, SliceRegion>> placed;
+  auto placements_of = [&](const HetAnnotation& a, const Shape& shape) -> const std::map<DeviceId, SliceRegion>& {
+    std::string key = a.str();
+    key += '@';
+    key += join_ints(shape);
+    auto it = placed.find(key);
+    if (it == placed.end()) it = placed.emplace(std::move(key), placements(a, shape)).first;
+    return it->second;
+  };
   auto add_state = [&](int state, int t, const HetAnnotation& a, const size_t* offs,
                        const void* const* ptrs = nullptr) {
-    for (const auto& [d, reg] : placements(a, shapes_[t])) {
+    for (const auto& [d, reg] : placements_of(a, shapes_[t])) {
       if (d < 0 || d >= n_virt_)
         fail(Errc::UnknownDevice, "device " + std::to_string(d) + " has no rank mapping");
       ShardLoc L;
@@ -158,7 +170,10 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
 }
 
 Program::~Program() {
-  if (dev_block_) cudaFree(dev_block_);
+  if (dev_block_) {
+    cudaDeviceSynchronize();  // no launch may still read the tables
+    ctx_.table_free(dev_block_);
+  }
   for (cudaEvent_t e : host_ev_)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ce_events_) cudaEventDestroy(e);
@@ -968,23 +983,33 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
 
 // ---------------------------------------------------------------- output merging
 std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks) {
-  std::map<std::string, int> index;
+  // key: the task's inputs (phase, tensor, rank, box, terms, groups) as raw words
+  std::unordered_map<std::string, int> index;
+  index.reserve(tasks.size() * 2);
   std::vector<BoxTask> out;
+  out.reserve(tasks.size());
+  std::string k;
+  auto put = [&k](int64_t v) { k.append(reinterpret_cast<const char*>(&v), sizeof v); };
   for (BoxTask& t : tasks) {
-    std::ostringstream k;
-    k << t.phase << '|' << t.tensor << '|' << t.rank << '|';
-    for (const auto& b : t.box.bounds) k << b[0] << ',' << b[1] << ';';
-    k << '|';
-    for (const Operand& o : t.terms) k << o.state << ':' << o.dev << ',';
-    k << '|';
-    for (int g : t.groups) k << g << ',';
-    auto it = index.find(k.str());
+    k.clear();
+    put(t.phase);
+    put(t.tensor);
+    put(t.rank);
+    put(static_cast<int64_t>(t.box.bounds.size()));
+    for (const auto& b : t.box.bounds) {
+      put(b[0]);
+      put(b[1]);
+    }
+    put(static_cast<int64_t>(t.terms.size()));
+    for (const Operand& o : t.terms) put((static_cast<int64_t>(o.state) << 32) | static_cast<uint32_t>(o.dev));
+    for (int g : t.groups) put(g);
+    auto it = index.find(k);
     if (it != index.end() && out[it->second].dsts.size() < static_cast<size_t>(kMaxOuts)) {
       BoxTask& m = out[it->second];
       m.dsts.insert(m.dsts.end(), t.dsts.begin(), t.dsts.end());
       continue;
     }
-    index[k.str()] = static_cast<int>(out.size());
+    index[k] = static_cast<int>(out.size());
     out.push_back(std::move(t));
   }
   return out;
@@ -1356,8 +1381,9 @@ Program::Flat Program::flatten(const BoxTask& bt) {
   return f;
 }
 
-bool Program::tma_capable(const BoxTask& bt) {
-  const Flat f = flatten(bt);
+bool Program::tma_capable(const BoxTask& bt) { return tma_capable(bt, flatten(bt)); }
+
+bool Program::tma_capable(const BoxTask& bt, const Flat& f) {
   bool all_local = true;
   for (const ShardLoc* L : f.locs) all_local = all_local && L->rank == bt.rank;
   return f.vec_bytes == 16 && (all_local || !(flags_ & HS_PROG_NO_TMA_PEER)) && !(flags_ & HS_PROG_NO_TMA) &&
@@ -1413,7 +1439,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       for (int j = 1; j < 4; ++j) tm.stride[j - 1] = j < rd ? f.st[k][rd - 1 - j] : 0;
       H.terms.push_back(tm);
     }
-    const bool tma = tma_capable(bt);
+    const bool tma = tma_capable(bt, f);
     if ((bt.wait >= 0 || !bt.targets.empty()) && !tma)
       fail(Errc::UnsupportedOp, "streamed task is not TMA-capable");  // lower() checks first
     const int32_t task_id = static_cast<int32_t>(H.tasks.size());
@@ -1599,7 +1625,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   clock_.mark("pack");
   char* base = nullptr;
   if (!ctx_.is_analysis()) {
-    cuda_check(cudaMalloc(&dev_block_, std::max<size_t>(total, 1)), "cudaMalloc(tables)");
+    dev_block_ = ctx_.table_alloc(total);
     cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
                "cudaMemcpy(tables)");
     base = static_cast<char*>(dev_block_);
@@ -1902,6 +1928,19 @@ std::string Program::stats_json() const {
   for (size_t i = 0; i < stats_.phase_bytes.size(); ++i)
     o << (i ? "," : "") << "[" << stats_.phase_bytes[i][0] << "," << stats_.phase_bytes[i][1] << ","
       << stats_.phase_bytes[i][2] << "]";
+  o << "],\"phase_kernels\":[";  // kernel of each launch, per launched phase
+  for (size_t p = 0; p < dphases_.size(); ++p) {
+    o << (p ? "," : "") << "[";
+    for (size_t i = 0; i < dphases_[p].launches.size(); ++i) {
+      const Launch& l = dphases_[p].launches[i];
+      const char* name = !l.tma                                      ? "box_phase_kernel"
+                         : l.tables.sigs                             ? "box_phase_tma_kernel"
+                         : l.tables.n_static >= l.tables.n_items     ? "box_phase_tma_static_kernel"
+                                                                     : "box_phase_tma_tail_kernel";
+      o << (i ? "," : "") << "\"" << name << "\"";
+    }
+    o << "]";
+  }
   o << "],\"dtype\":" << dtype_ << ",\"rank\":" << ctx_.rank() << "}";
   return o.str();
 }

@@ -82,6 +82,13 @@ class Context {
   void ipc_export(const void* ptr, unsigned char out[80]) const;
   char* ipc_import(const unsigned char in[80]);
 
+  // Device memory for program tables: first-fit in a pool reserved with the
+  // context (HS_TABLE_POOL_MB, default 1024), so compiling a program does not
+  // pay cudaMalloc (3-16 ms measured for a cfg4 switch's 35 MB of records);
+  // beyond the pool, cudaMalloc.
+  void* table_alloc(size_t bytes);
+  void table_free(void* p);
+
   // NCCL communicator over the same ranks (HS_PROG_NCCL baseline transport).
   void nccl_init(const unsigned char id[128]);
   void* nccl_comm() const { return nccl_comm_; }
@@ -99,6 +106,10 @@ class Context {
   std::vector<char*> peer_arena_;
   std::vector<unsigned int*> peer_flags_;
   std::map<std::string, char*> imported_;  // IPC handle bytes -> mapped base
+  char* pool_ = nullptr;                    // table pool
+  size_t pool_bytes_ = 0;
+  std::map<size_t, size_t> pool_free_;      // offset -> bytes (coalesced)
+  std::map<size_t, size_t> pool_used_;      // offset -> bytes
   unsigned int epoch_ = 0;
   bool peers_open_ = false;
   cudaStream_t stream_ = nullptr;
@@ -232,6 +243,7 @@ class Program {
   struct Flat;
   Flat flatten(const BoxTask& bt);
   bool tma_capable(const BoxTask& bt);
+  bool tma_capable(const BoxTask& bt, const Flat& f);
   void build_tables(const std::vector<BoxTask>& tasks);
   ShardLoc& loc(int state, int tensor, DeviceId d);
   char* addr_of(const ShardLoc& L) const { return L.ptr ? L.ptr : ctx_.arena_of(L.rank) + L.offset; }

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <string>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 
@@ -37,14 +39,30 @@ SwitchPlan plan_switch(const std::vector<SwitchEntry>& diff, DType dtype,
   SwitchPlan sp;
   sp.diff = diff;
   sp.dtype = dtype;
-  // build_table per parameter, sequentially: 1.2 ms for cfg4's 291 tables on
-  // one thread; a thread pool measured slower (thread start-up and allocator
-  // contention exceed the work).
+  // build_table per parameter.  A model's parameters repeat a handful of
+  // (src, dst, shape) triples (cfg4: 291 tensors, 12 triples), and a table
+  // depends on the tensor only through BsrRow::tensor_id, so each distinct
+  // triple is built once and its rows relabelled (same table, same order).
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<BsrTable> tables;
   tables.reserve(diff.size());
-  for (const SwitchEntry& e : diff)
-    tables.push_back(build_table(e.src, e.dst, e.shape, e.tensor_id, dtype_width(dtype)));
+  std::unordered_map<std::string, size_t> seen;  // triple -> index of its first table
+  for (const SwitchEntry& e : diff) {
+    std::string key = e.src.str();
+    key += '>';
+    key += e.dst.str();
+    key += '@';
+    key += join_ints(e.shape);
+    auto it = seen.find(key);
+    if (it == seen.end()) {
+      seen.emplace(std::move(key), tables.size());
+      tables.push_back(build_table(e.src, e.dst, e.shape, e.tensor_id, dtype_width(dtype)));
+    } else {
+      BsrTable t = tables[it->second];
+      for (BsrRow& r : t.rows) r.tensor_id = e.tensor_id;
+      tables.push_back(std::move(t));
+    }
+  }
   const auto t1 = std::chrono::steady_clock::now();
   sp.plan = fuse(tables, bandwidth);
   if (std::getenv("HS_COMPILE_TRACE"))

@@ -562,7 +562,10 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_FANOUT_ONCE | HS_PROG_NO_SHARE,
                        HS_PROG_PULL_MID | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL,
                        HS_PROG_NO_SHARE | HS_PROG_BULK_STORE,
-                       HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_BULK_STORE]
+                       HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_BULK_STORE,
+                       # relays pushed while local groups reduce, then a short consume phase
+                       HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM,
+                       HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_NO_SHARE]
 AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE, HS_PROG_SMALL_ITEMS, HS_PROG_SMALL_ITEMS | HS_PROG_BULK_STORE]
 TUNE_MARGIN = 0.01  # a later candidate must beat the best so far by 1% (timing noise)
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every
