@@ -408,13 +408,15 @@ def main():
         return prog.flags  # what autotune returned (its 1% margin can keep an earlier candidate)
 
     def timed(prog, steps, warmup, profile=False):
+        """Device ms per step over `steps` back-to-back runs (CUDA events on the launching
+        stream, max over ranks); with profile=True a second, separate pass records each
+        launched phase's duration (per-phase events would split the back-to-back launches
+        that programmatic dependent launch overlaps, so the step time is taken without them)."""
         for _ in range(warmup):
             prog.run(sp)
         stream.synchronize()
         ctx.sync()
         barrier()
-        if profile:
-            prog.profile(True)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             a.record()
@@ -427,9 +429,15 @@ def main():
         ms = a.elapsed_time(b) / steps
         phase = None
         if profile:
+            prog.profile(True)
+            for _ in range(min(steps, 50)):
+                prog.run(sp)
+            stream.synchronize()
+            ctx.sync()
             phase, runs = prog.phase_ms()
             phase = [x / max(1, runs) for x in phase]
             prog.profile(False)
+            barrier()
         return allreduce_max(ms), phase
 
     if args.sweep:

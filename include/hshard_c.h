@@ -165,9 +165,12 @@ enum {
   HS_PROG_SEPARATE_BARRIERS = 1 << 26, /* world > 1: every cross-rank barrier is its own launch
                                      (default: folded into the prologue of the phase's first
                                      launch when that is a TMA kernel) */
-  HS_PROG_SMALL_ITEMS = 1 << 27   /* 16 KB TMA work items instead of 32 KB: plan-dependent (faster
+  HS_PROG_SMALL_ITEMS = 1 << 27,  /* 16 KB TMA work items instead of 32 KB: plan-dependent (faster
                                      for two-output copies, slower for long single-output ones) --
                                      the autotuner times it */
+  HS_PROG_NO_PDL = 1 << 28        /* launch phase kernels without programmatic dependent launch
+                                     (default: each launch is scheduled while the previous one on
+                                     the stream drains and waits for it on the device) */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

@@ -265,11 +265,24 @@ __device__ __forceinline__ RowPtr row_ptr(const TermDesc& t, const WorkItem& w, 
 }
 
 // ---------------------------------------------------------------- register path
+// Programmatic dependent launch (PhaseTables::pdl): every phase kernel lets
+// the next launch on its stream be scheduled at once (its CTAs take SMs as
+// this grid's CTAs retire and run their prologue), and waits -- before its
+// first access to memory an earlier kernel may write, and before announcing
+// a folded cross-rank barrier -- until every earlier grid on the stream has
+// completed with its memory visible (griddepcontrol.wait).  Without the
+// launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <class T, int VB, bool kReduce>
 __global__ void __launch_bounds__(kBlock, kReduce ? 1 : 2) box_phase_kernel(PhaseTables t) {
   __shared__ RowPtr ops[kMaxTerms + kMaxOuts];
   __shared__ TaskDesc task_s;
   using R = typename Raw<VB>::type;
+  pdl_begin();
   for (int it = blockIdx.x; it < t.n_items; it += gridDim.x) {
     const WorkItem w = t.items[it];
     __syncthreads();  // previous item done with ops / task_s
@@ -752,6 +765,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) box_phase_tma_kernel(PhaseTabl
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_begin();
   if (t.bar_flags) {  // folded cross-rank barrier (replaces a barrier launch)
     volatile int* ok = reinterpret_cast<volatile int*>(meta);  // unused until the first item
     if (threadIdx.x == 0) *ok = folded_barrier(t.bar_flags, t.bar_world, t.bar_rank, t.bar_epoch, t.error);
@@ -939,6 +953,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_tail_kernel(Phas
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_begin();
   if (t.bar_flags) {  // folded cross-rank barrier (replaces a barrier launch)
     volatile int* ok = reinterpret_cast<volatile int*>(meta);  // unused until the first item
     if (threadIdx.x == 0) *ok = folded_barrier(t.bar_flags, t.bar_world, t.bar_rank, t.bar_epoch, t.error);
@@ -1035,6 +1050,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) box_phase_tma_static_kernel(Ph
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_begin();
   if (t.bar_flags) {  // folded cross-rank barrier (replaces a barrier launch)
     volatile int* ok = reinterpret_cast<volatile int*>(meta);  // unused until the first item
     if (threadIdx.x == 0) *ok = folded_barrier(t.bar_flags, t.bar_world, t.bar_rank, t.bar_epoch, t.error);
@@ -1295,20 +1311,36 @@ constexpr size_t kTmaSmem = kTmaStages * kStageBytes + kTmaStages * 32 * sizeof(
                             2 * kTmaStages * sizeof(uint64_t);
 constexpr size_t kDynSmem = kTmaSmem + sizeof(SigRing);
 
+// Phase kernels launch with the programmatic-stream-serialization attribute
+// when the program asks for it (see pdl_begin).
+inline void launch_k(void (*k)(PhaseTables), dim3 g, dim3 b, size_t smem, cudaStream_t s, const PhaseTables& t) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = t.pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, t);
+}
+
 template <class T>
 struct PhaseK {
   template <bool R>
   static void reg(dim3 g, dim3 b, cudaStream_t s, PhaseTables t, int vb) {
     switch (vb) {
-      case 16: box_phase_kernel<T, 16, R><<<g, b, 0, s>>>(t); break;
+      case 16: launch_k(box_phase_kernel<T, 16, R>, g, b, 0, s, t); break;
       case 8:
-        if constexpr (sizeof(T) <= 8) box_phase_kernel<T, 8, R><<<g, b, 0, s>>>(t);
+        if constexpr (sizeof(T) <= 8) launch_k(box_phase_kernel<T, 8, R>, g, b, 0, s, t);
         break;
       case 4:
-        if constexpr (sizeof(T) <= 4) box_phase_kernel<T, 4, R><<<g, b, 0, s>>>(t);
+        if constexpr (sizeof(T) <= 4) launch_k(box_phase_kernel<T, 4, R>, g, b, 0, s, t);
         break;
       case 2:
-        if constexpr (sizeof(T) <= 2) box_phase_kernel<T, 2, R><<<g, b, 0, s>>>(t);
+        if constexpr (sizeof(T) <= 2) launch_k(box_phase_kernel<T, 2, R>, g, b, 0, s, t);
         break;
     }
   }
@@ -1329,16 +1361,16 @@ struct PhaseK {
       }();
       (void)configured;
       if (t.sigs)  // streamed: ready flags, two queues, signaller warp
-        box_phase_tma_kernel<T><<<g, dim3(kDynThreads), kDynSmem, s>>>(t);
+        launch_k(box_phase_tma_kernel<T>, g, dim3(kDynThreads), kDynSmem, s, t);
       else if (t.n_static >= t.n_items)
         if (t.bulk_store)
-          box_phase_tma_static_kernel<T, true><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+          launch_k(box_phase_tma_static_kernel<T, true>, g, dim3(kTmaThreads), kTmaSmem, s, t);
         else
-          box_phase_tma_static_kernel<T, false><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+          launch_k(box_phase_tma_static_kernel<T, false>, g, dim3(kTmaThreads), kTmaSmem, s, t);
       else if (t.bulk_store)
-        box_phase_tma_tail_kernel<T, true><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+        launch_k(box_phase_tma_tail_kernel<T, true>, g, dim3(kTmaThreads), kTmaSmem, s, t);
       else
-        box_phase_tma_tail_kernel<T, false><<<g, dim3(kTmaThreads), kTmaSmem, s>>>(t);
+        launch_k(box_phase_tma_tail_kernel<T, false>, g, dim3(kTmaThreads), kTmaSmem, s, t);
       return;
     }
     if (reduce)

@@ -135,6 +135,7 @@ struct PhaseTables {
   unsigned int* const* bar_flags;    // every rank's flag array (peer-mapped), or null
   int32_t bar_world, bar_rank;
   uint32_t bar_epoch;
+  int32_t pdl;                       // launch with programmatic stream serialization (pdl_begin)
 };
 
 // Shared-memory staging of the TMA kernel: kStages ring buffers of

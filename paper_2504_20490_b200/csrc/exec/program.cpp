@@ -1661,6 +1661,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables.first_ctas = l.grid;
       l.tables.error = ctx_.error_flag();
       l.tables.bulk_store = (flags_ & HS_PROG_BULK_STORE) ? kBulkStoreOutputs : 0;
+      l.tables.pdl = !(flags_ & HS_PROG_NO_PDL) && !ce_mode_;
       if (l.tma && std::getenv("HS_TRACE") && !ctx_.is_analysis()) {
         stats_.trace_off = ctx_.alloc(static_cast<size_t>(l.grid) * 64);
         stats_.trace_ctas = l.grid;

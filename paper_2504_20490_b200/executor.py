@@ -46,6 +46,7 @@ HS_PROG_STATIC_LOCAL = 1 << 24  # world > 1: static dealing for uniform local-on
 HS_PROG_BULK_STORE = 1 << 25  # static TMA kernel: copies' first two outputs leave through TMA bulk stores
 HS_PROG_SEPARATE_BARRIERS = 1 << 26  # world > 1: barriers as their own launches, not kernel prologues
 HS_PROG_SMALL_ITEMS = 1 << 27  # 16 KB TMA work items (plan-dependent; autotuned at N=1)
+HS_PROG_NO_PDL = 1 << 28  # no programmatic dependent launch between phase kernels (A/B)
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
