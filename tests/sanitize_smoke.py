@@ -1,6 +1,8 @@
-"""Small executor workloads for compute-sanitizer (memcheck / racecheck):
-the fused TMA kernel (cfg2e shape), the register path (unaligned boxes),
-a switch plan, fill and verify kernels.  Exit code 0 = all results correct."""
+"""Small executor workloads for compute-sanitizer (memcheck / racecheck /
+synccheck): the fused TMA kernel (cfg2e shape), the register path (unaligned
+boxes), TMA bulk stores and small items, back-to-back runs with programmatic
+dependent launch, a switch plan (device-expanded records), fill and verify
+kernels.  Exit code 0 = all results correct."""
 import os
 import sys
 
@@ -22,12 +24,13 @@ cases.append(("hsize=2 hdim=-2 [(0,1){0:2}; (2,3){0:2}]", "hsize=2 hdim=-1 [(0,1
 bad = 0
 for src, dst, shape, dt in cases:
     plan = H.classify(src, dst, shape, dt)
-    for flags in (0, 14):
+    for flags in (0, 14, (1 << 25) | (1 << 27)):
         mark = ctx.alloc(0)
         lay = ShardLayout(ctx, plan, 8)
         lay.fill_src(5, "real" if dt != "i32" else "grid")
         prog = Program(ctx, plan, lay, flags)
-        prog.run()
+        for _ in range(3):  # back to back: programmatic dependent launch between runs
+            prog.run()
         ctx.sync()
         want = ox.execute_plan(plan.json(), ox.scatter(src, shape, dt, 5, 0, "real"), dt)
         for (slot, dev) in lay.dst:
