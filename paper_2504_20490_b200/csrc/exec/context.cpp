@@ -41,57 +41,71 @@ Context::Context(int rank, int world, int gpu, size_t arena_bytes)
                         cudaMemcpyHostToDevice),
              "cudaMemcpy(peers)");
   const char* pool_mb = std::getenv("HS_TABLE_POOL_MB");
-  pool_bytes_ = static_cast<size_t>(pool_mb ? std::atoll(pool_mb) : 1024) << 20;
-  if (pool_bytes_ && cudaMalloc(&pool_, pool_bytes_) == cudaSuccess) {
-    pool_free_[0] = pool_bytes_;
-  } else {
-    cudaGetLastError();  // no pool: every table block is a cudaMalloc
-    pool_ = nullptr;
-    pool_bytes_ = 0;
-  }
+  pool_ = std::make_shared<TablePool>(gpu, static_cast<size_t>(pool_mb ? std::atoll(pool_mb) : 1024) << 20);
   cuda_check(cudaDeviceSynchronize(), "context init");
 }
 
-void* Context::table_alloc(size_t bytes) {
+TablePool::TablePool(int gpu, size_t bytes) : gpu_(gpu) {
+  if (bytes && cudaMalloc(&base_, bytes) == cudaSuccess) {
+    bytes_ = bytes;
+    free_[0] = bytes;
+  } else {
+    cudaGetLastError();  // no pool: every table block is a cudaMalloc
+    base_ = nullptr;
+  }
+}
+
+TablePool::~TablePool() {
+  if (base_) {
+    cudaSetDevice(gpu_);
+    cudaFree(base_);
+  }
+}
+
+void* TablePool::alloc(size_t bytes) {
   bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t{255};
-  for (auto it = pool_free_.begin(); it != pool_free_.end(); ++it)
-    if (it->second >= bytes) {
-      const size_t off = it->first, left = it->second - bytes;
-      pool_free_.erase(it);
-      if (left) pool_free_[off + bytes] = left;
-      pool_used_[off] = bytes;
-      return pool_ + off;
-    }
+  {
+    std::lock_guard<std::mutex> lock(mu_);
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+      if (it->second >= bytes) {
+        const size_t off = it->first, left = it->second - bytes;
+        free_.erase(it);
+        if (left) free_[off + bytes] = left;
+        used_[off] = bytes;
+        return base_ + off;
+      }
+  }
   void* p = nullptr;
   cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(tables)");
   return p;
 }
 
-void Context::table_free(void* p) {
+void TablePool::free(void* p) {
   char* c = static_cast<char*>(p);
-  if (!pool_ || c < pool_ || c >= pool_ + pool_bytes_) {
+  if (!base_ || c < base_ || c >= base_ + bytes_) {
     cudaFree(p);
     return;
   }
-  const size_t off = static_cast<size_t>(c - pool_);
-  auto u = pool_used_.find(off);
-  if (u == pool_used_.end()) return;
+  std::lock_guard<std::mutex> lock(mu_);
+  const size_t off = static_cast<size_t>(c - base_);
+  auto u = used_.find(off);
+  if (u == used_.end()) return;
   size_t start = off, len = u->second;
-  pool_used_.erase(u);
-  auto next = pool_free_.lower_bound(start);
-  if (next != pool_free_.end() && next->first == start + len) {
+  used_.erase(u);
+  auto next = free_.lower_bound(start);
+  if (next != free_.end() && next->first == start + len) {
     len += next->second;
-    next = pool_free_.erase(next);
+    next = free_.erase(next);
   }
-  if (next != pool_free_.begin()) {
+  if (next != free_.begin()) {
     auto prev = std::prev(next);
     if (prev->first + prev->second == start) {
       start = prev->first;
       len += prev->second;
-      pool_free_.erase(prev);
+      free_.erase(prev);
     }
   }
-  pool_free_[start] = len;
+  free_[start] = len;
 }
 
 Context::Context(AnalysisTag, int rank, int world) : rank_(rank), world_(world), gpu_(-1) {
@@ -120,7 +134,7 @@ Context::~Context() {
     if (peer_arena_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
     if (peer_flags_[r]) cudaIpcCloseMemHandle(peer_flags_[r]);
   }
-  if (pool_) cudaFree(pool_);
+  pool_.reset();  // the device block goes with the last program still holding it
   cudaFree(d_peer_flags_);
   cudaFree(counter_);
   cudaFree(barrier_error_);

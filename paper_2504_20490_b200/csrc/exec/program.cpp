@@ -172,7 +172,7 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
 Program::~Program() {
   if (dev_block_) {
     cudaDeviceSynchronize();  // no launch may still read the tables
-    ctx_.table_free(dev_block_);
+    pool_->free(dev_block_);  // (the context itself may already be gone)
   }
   for (cudaEvent_t e : host_ev_)
     if (e) cudaEventDestroy(e);
@@ -1625,7 +1625,8 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   clock_.mark("pack");
   char* base = nullptr;
   if (!ctx_.is_analysis()) {
-    dev_block_ = ctx_.table_alloc(total);
+    pool_ = ctx_.tables();
+    dev_block_ = pool_->alloc(total);
     cuda_check(cudaMemcpy(dev_block_, host.data(), host.size(), cudaMemcpyHostToDevice),
                "cudaMemcpy(tables)");
     base = static_cast<char*>(dev_block_);

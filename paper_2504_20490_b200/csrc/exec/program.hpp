@@ -10,6 +10,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -33,6 +34,27 @@ struct StageClock {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+
+// Device memory for program tables: first-fit in a block reserved with the
+// context (HS_TABLE_POOL_MB, default 1024), so compiling a program does not
+// pay cudaMalloc (3-16 ms measured for a cfg4 switch's 35 MB of records);
+// beyond the block, cudaMalloc.  Owned jointly by the context and its
+// programs: freed when the last of them goes.
+class TablePool {
+ public:
+  TablePool(int gpu, size_t bytes);
+  ~TablePool();
+  void* alloc(size_t bytes);
+  void free(void* p);
+
+ private:
+  std::mutex mu_;
+  int gpu_;
+  char* base_ = nullptr;
+  size_t bytes_ = 0;
+  std::map<size_t, size_t> free_;  // offset -> bytes (coalesced)
+  std::map<size_t, size_t> used_;  // offset -> bytes
+};
 
 // Per-GPU context: one per process ("rank").  Owns the symmetric arena, the
 // barrier flag block and (after open_peers) every peer's mapped arena.
@@ -82,12 +104,9 @@ class Context {
   void ipc_export(const void* ptr, unsigned char out[80]) const;
   char* ipc_import(const unsigned char in[80]);
 
-  // Device memory for program tables: first-fit in a pool reserved with the
-  // context (HS_TABLE_POOL_MB, default 1024), so compiling a program does not
-  // pay cudaMalloc (3-16 ms measured for a cfg4 switch's 35 MB of records);
-  // beyond the pool, cudaMalloc.
-  void* table_alloc(size_t bytes);
-  void table_free(void* p);
+  // Device memory for program tables (TablePool, shared with the programs so
+  // that a program destroyed after its context still frees correctly).
+  const std::shared_ptr<TablePool>& tables() const { return pool_; }
 
   // NCCL communicator over the same ranks (HS_PROG_NCCL baseline transport).
   void nccl_init(const unsigned char id[128]);
@@ -106,10 +125,7 @@ class Context {
   std::vector<char*> peer_arena_;
   std::vector<unsigned int*> peer_flags_;
   std::map<std::string, char*> imported_;  // IPC handle bytes -> mapped base
-  char* pool_ = nullptr;                    // table pool
-  size_t pool_bytes_ = 0;
-  std::map<size_t, size_t> pool_free_;      // offset -> bytes (coalesced)
-  std::map<size_t, size_t> pool_used_;      // offset -> bytes
+  std::shared_ptr<TablePool> pool_;
   unsigned int epoch_ = 0;
   bool peers_open_ = false;
   cudaStream_t stream_ = nullptr;
@@ -264,6 +280,7 @@ class Program {
   int n_phases_ = 0;
   std::vector<DevicePhase> dphases_;
   void* dev_block_ = nullptr;
+  std::shared_ptr<TablePool> pool_;  // dev_block_'s owner
   bool profiling_ = false;
   bool remote_final_writes_ = false;  // last phase stores into peers' shards
   bool streamed_ = false;             // both plan phases in one launch (ready flags)

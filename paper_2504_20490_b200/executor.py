@@ -17,6 +17,7 @@ import ctypes
 import json
 import os
 import time
+import weakref
 from ctypes import c_int, c_size_t, c_ulonglong, c_void_p
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -69,6 +70,7 @@ class Context:
         h = c_void_p()
         check(LIB.hs_ctx_create(rank, world, self.gpu, arena_bytes, ctypes.byref(h)))
         self._h = h
+        self._programs = weakref.WeakSet()
         base, size = c_void_p(), c_size_t()
         check(LIB.hs_ctx_arena(self._h, ctypes.byref(base), ctypes.byref(size)))
         self.arena_base, self.arena_bytes = base.value, size.value
@@ -138,6 +140,10 @@ class Context:
         check(LIB.hs_ctx_clear_error(self._h))
 
     def close(self) -> None:
+        # programs compiled against this context go first (their tables, events
+        # and streams belong to its device)
+        for prog in list(getattr(self, "_programs", ())):
+            prog.close()
         h, self._h = getattr(self, "_h", None), None
         if h:
             LIB.hs_ctx_destroy(h)
@@ -498,6 +504,7 @@ class Program:
             check(LIB.hs_prog_compile(ctx.handle, plan.handle, m, layout.n_virtual, layout.src_off,
                                       layout.dst_off, flags, ctypes.byref(h)))
         self._h = h
+        ctx._programs.add(self)
 
     def run(self, stream=None) -> None:
         check(LIB.hs_prog_run(self._h, stream))
