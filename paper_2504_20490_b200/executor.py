@@ -322,8 +322,10 @@ class StateLayout:
         self.base = ctx.alloc(self.size) if base is None else int(base)
         if self.base + self.size > ctx.arena_bytes:
             raise H.HshardError("ShapeMismatch", "state does not fit the arena")
+        self._by_tid: Dict[int, Dict[int, int]] = {}
         for rec in self.recs.values():
             rec["offset"] = self.base + rec["rel"]
+            self._by_tid.setdefault(rec["tid"], {})[rec["dev"]] = rec["offset"]
 
     @staticmethod
     def _pack(entries, es, n_virtual, v_to_rank, world):
@@ -355,15 +357,12 @@ class StateLayout:
     def offsets(self, tensor_ids: Sequence[int]):
         """Offset table for a plan whose tensor slots are `tensor_ids` (slot i = the plan's
         i-th tensor): arr[i * n_virtual + dev]; tensors this state lacks stay absent."""
-        by_tid = {}
-        for (slot, dev), rec in self.recs.items():
-            by_tid.setdefault(rec["tid"], {})[dev] = rec["offset"]
-        n = len(tensor_ids) * self.n_virtual
-        arr = (c_size_t * max(1, n))(*([SIZE_MAX] * max(1, n)))
+        nv = self.n_virtual
+        flat = np.full(max(1, len(tensor_ids) * nv), SIZE_MAX, dtype=np.uint64)
         for i, tid in enumerate(tensor_ids):
-            for dev, off in by_tid.get(int(tid), {}).items():
-                arr[i * self.n_virtual + dev] = off
-        return arr
+            for dev, off in self._by_tid.get(int(tid), {}).items():
+                flat[i * nv + dev] = off
+        return flat
 
     def local(self):
         return {k: v for k, v in self.recs.items() if v["rank"] == self.ctx.rank}
@@ -402,7 +401,8 @@ class Transition:
         else:
             tids = [int(e[0]) for e in plan.meta["entries"]]
         self.entries = [(t, None, None, None) for t in tids]
-        self.src_off, self.dst_off = src.offsets(tids), dst.offsets(tids)
+        self._offs = (src.offsets(tids), dst.offsets(tids))  # kept alive for the pointers
+        self.src_off, self.dst_off = (a.ctypes.data_as(ctypes.POINTER(c_size_t)) for a in self._offs)
 
 
 class SwitchCache:
@@ -416,9 +416,15 @@ class SwitchCache:
         self.ctx = ctx
         self.plans: Dict[tuple, "H.Plan"] = {}
         self.programs: Dict[tuple, "Program"] = {}
+        self._by_id: Dict[tuple, tuple] = {}  # (id(entries), dtype) -> (entries, key)
 
     def plan(self, entries, dtype: str):
+        # the same entries object again (a cycle's step lists): no key rebuild
+        ident = self._by_id.get((id(entries), dtype))
+        if ident is not None and ident[0] is entries:
+            return self.plans[ident[1]], True
         key = (tuple((int(t), s, d, tuple(int(x) for x in sh)) for t, s, d, sh in entries), dtype)
+        self._by_id[(id(entries), dtype)] = (entries, key)
         p = self.plans.get(key)
         hit = p is not None
         if not hit:
@@ -438,6 +444,7 @@ class SwitchCache:
             p.close()
         self.programs.clear()
         self.plans.clear()
+        self._by_id.clear()
 
 
 class StrategyCycle:
