@@ -1,3 +1,8 @@
+// PORT NOTICE: this file is a port of the reference planner's src/bsr.cpp
+// (hshard, Copyright 2026 The hshard Authors, Apache License 2.0 -- see
+// NOTICE): the same algorithm statement for statement, with renamed
+// identifiers, so that plans are byte-identical to the reference's.
+//
 // hshard-b200 planner: BSR tables, heuristic sender selection, fusion.
 //
 // Follows the reference bsr.cpp: finest-slice grid over the scope

@@ -1,3 +1,8 @@
+// PORT NOTICE: this file is a port of the reference planner's src/common.cpp
+// (hshard, Copyright 2026 The hshard Authors, Apache License 2.0 -- see
+// NOTICE): the same algorithm statement for statement, with renamed
+// identifiers, so that plans are byte-identical to the reference's.
+//
 // hshard-b200 planner: dtypes, error names, exact rationals.
 // Behaviour follows the reference common.cpp:22-146 (widths, names, rational
 // normalisation, floor_mul); BF16 is an appended dtype (width 2).
