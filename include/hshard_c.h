@@ -52,6 +52,13 @@ int hs_plan_switch(int n, const int* tensor_ids, const char* const* src, const c
 int hs_plan_dump(const hs_plan* plan, char** json);
 void hs_plan_destroy(hs_plan* plan);
 
+/* volume_report(plan, node_of)                     reference bsr.hpp:107-108
+ * Per-sender intra-/inter-node transfer bytes (the paper's Table 3 shape) of a
+ * switch's fused BsrPlan (or of every Bsr step of a CommPlan); node_of is
+ * devices[i] -> nodes[i] for i < n.  -> JSON {"device": [intra, inter], ...}
+ * with every device of node_of present; UnknownDevice for a transfer end
+ * outside it. */
+int hs_volume_report(const hs_plan* plan, int n, const int* devices, const int* nodes, char** json);
 /* build_table(...) dump                                reference bsr.hpp:50-51 */
 int hs_build_table(const char* src, const char* dst, const int64_t* shape, int ndim,
                    int tensor_id, int elem_bytes, char** json);

@@ -20,6 +20,7 @@
 //   T|elem_bytes|shape|tid|src|dst            build_table       -> table JSON
 //   M|bw|naive|elem_bytes|shape|src|dst       make_plan(_naive) -> bsr JSON
 //   F|bw|n  + n lines  tid|elem_bytes|shape|src|dst   fuse      -> bsr JSON
+//   R|bw|n|d:node,...  + n lines (as F)         fuse + volume_report
 //   P|shape|anno                              placement of every device
 //   H|anno|target                             convert_hsize
 //   Q|anno|anno                               annotations_equal
@@ -740,6 +741,29 @@ std::string handle(const std::string& line, std::istream& in) {
                                    std::stoi(g.at(0)), std::stoi(g.at(1))));
     }
     return jbsr(fuse(tables, bw));
+  }
+  if (c == "R") {  // R|bw|n|d:node,d:node,...  + n lines tid|elem_bytes|shape|src|dst
+    Bandwidth bw = parse_bw(f.at(1));
+    int n = std::stoi(f.at(2));
+    std::map<DeviceId, int> node_of;
+    for (auto& kv : split(trim(f.at(3)), ','))
+      if (!trim(kv).empty()) node_of[std::stoi(split(kv, ':').at(0))] = std::stoi(split(kv, ':').at(1));
+    std::vector<BsrTable> tables;
+    std::vector<std::string> lines(n);
+    for (int i = 0; i < n; ++i) std::getline(in, lines[i]);
+    for (int i = 0; i < n; ++i) {
+      auto g = split(lines[i], '|');
+      tables.push_back(build_table(parse_anno(g.at(3)), parse_anno(g.at(4)), parse_shape(g.at(2)),
+                                   std::stoi(g.at(0)), std::stoi(g.at(1))));
+    }
+    std::string o = "{";
+    bool first = true;
+    for (const auto& [d, v] : volume_report(fuse(tables, bw), node_of)) {
+      o += std::string(first ? "" : ",") + "\"" + std::to_string(d) + "\":[" + std::to_string(v.intra_bytes) +
+           "," + std::to_string(v.inter_bytes) + "]";
+      first = false;
+    }
+    return o + "}";
   }
   if (c == "P") {
     Shape shape = parse_shape(f.at(1));

@@ -90,6 +90,7 @@ def _load() -> ctypes.CDLL:
         "hs_ctx_sync": (c_int, [c_void_p]),
         "hs_ctx_barrier": (c_int, [c_void_p, c_void_p]),
         "hs_ctx_clear_error": (c_int, [c_void_p]),
+        "hs_volume_report": (c_int, [c_void_p, c_int, P(c_int), P(c_int), P(c_void_p)]),
         "hs_prog_compile_ptrs": (c_int, [c_void_p, c_void_p, P(c_int), c_int, P(c_void_p), P(c_void_p), c_int,
                                          P(c_void_p)]),
         "hs_ipc_export": (c_int, [c_void_p, c_void_p, c_char_p]),

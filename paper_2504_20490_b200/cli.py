@@ -93,7 +93,9 @@ def cmd_switch_plan(a):
     plan = H.plan_switch([(e["tensor"], e["src"], e["dst"], tuple(e["shape"])) for e in entries], a.dtype,
                          a.bandwidth)
     pj = json.loads(plan.dump())
-    vol = F.volume_report(pj["xfer"], a.devices_per_node)
+    devs = sorted({d for e in entries for an in (e["src"], e["dst"])
+                   for g in H.parse_annotation(an)["groups"] for d in g})
+    vol = H.volume_report(plan, {d: d // a.devices_per_node for d in devs})  # reference bsr.cpp:244-261
     rows = [(d, f"{v[0] / 2**20:.1f}", f"{v[1] / 2**20:.1f}") for d, v in vol.items()]
     _emit({"version": F.VERSION, "kind": "switch", "strategies": [sa, sb], "dtype": a.dtype,
            "entries": [{**e, "src": F.anno_to_json(e["src"]), "dst": F.anno_to_json(e["dst"])} for e in entries],

@@ -96,6 +96,29 @@ int hs_plan_dump(const hs_plan* plan, char** json) {
 
 void hs_plan_destroy(hs_plan* plan) { delete plan; }
 
+int hs_volume_report(const hs_plan* plan, int n, const int* devices, const int* nodes, char** json) {
+  return guarded([&] {
+    std::map<DeviceId, int> node_of;
+    for (int i = 0; i < n; ++i) node_of[devices[i]] = nodes[i];
+    BsrPlan merged;  // a switch's fused plan, or every Bsr step of a CommPlan
+    if (plan->sw) {
+      merged = plan->sw->plan;
+    } else {
+      for (const auto* ph : {&plan->comm->bottom_phase, &plan->comm->top_phase})
+        for (const CommStep& st : *ph)
+          if (st.bsr) merged.transfers.insert(merged.transfers.end(), st.bsr->transfers.begin(), st.bsr->transfers.end());
+    }
+    std::string o = "{";
+    bool first = true;
+    for (const auto& [d, v] : volume_report(merged, node_of)) {
+      o += std::string(first ? "" : ",") + "\"" + std::to_string(d) + "\":[" + std::to_string(v.intra_bytes) + "," +
+           std::to_string(v.inter_bytes) + "]";
+      first = false;
+    }
+    *json = capi::dup_string(o + "}");
+  });
+}
+
 int hs_build_table(const char* src, const char* dst, const int64_t* shape, int ndim,
                    int tensor_id, int elem_bytes, char** json) {
   return guarded([&] {

@@ -20,7 +20,7 @@ from __future__ import annotations
 import json
 import struct
 from fractions import Fraction
-from typing import Dict, List, Sequence
+from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
@@ -146,13 +146,22 @@ def read_tensor(path: str):
 
 
 # ---------------------------------------------------------------- reports
-def volume_report(xfer: Sequence, devices_per_node: int = 8) -> Dict[int, List[int]]:
-    """Per sender: [intra-node bytes, inter-node bytes] (reference volume_report, bsr.hpp:107-108)."""
-    out: Dict[int, List[int]] = {}
+def volume_report(xfer: Sequence, devices_per_node: int = 8, node_of: Optional[Dict[int, int]] = None
+                  ) -> Dict[int, List[int]]:
+    """The reference volume_report (bsr.hpp:107-108, bsr.cpp:244-261) over a plan JSON's
+    transfers: {device: [intra-node bytes, inter-node bytes]} with every device of
+    `node_of` present (zeros included), UnknownDevice for a transfer end outside it.
+    Without node_of, the devices the transfers touch on nodes of `devices_per_node`."""
+    if node_of is None:
+        devs = {int(x[i]) for x in xfer for i in (2, 3)}
+        node_of = {d: d // devices_per_node for d in devs}
+    out: Dict[int, List[int]] = {d: [0, 0] for d in node_of}
     for x in xfer:
         s, r, b = int(x[2]), int(x[3]), int(x[4])
-        row = out.setdefault(s, [0, 0])
-        row[0 if s // devices_per_node == r // devices_per_node else 1] += b
+        for d, role in ((s, "sender"), (r, "receiver")):
+            if d not in node_of:
+                raise H.HshardError("UnknownDevice", f"{role} {d} not in cluster")
+        out[s][0 if node_of[s] == node_of[r] else 1] += b
     return dict(sorted(out.items()))
 
 

@@ -146,3 +146,15 @@ def align_shard_specs(a, b):
     out = c_void_p()
     check(LIB.hs_align_shard_specs(_ds_str(a).encode(), _ds_str(b).encode(), ctypes.byref(out)))
     return json.loads(take_string(out))
+
+
+def volume_report(plan: "Plan", node_of: Dict[int, int]) -> Dict[int, List[int]]:
+    """Reference volume_report (bsr.hpp:107-108, bsr.cpp:244-261) through the C ABI:
+    {device: [intra-node bytes, inter-node bytes]} over the plan's transfers."""
+    devs = sorted(node_of)
+    n = len(devs)
+    d = (c_int * max(1, n))(*devs)
+    nd = (c_int * max(1, n))(*[node_of[x] for x in devs])
+    out = c_void_p()
+    check(LIB.hs_volume_report(plan.handle, n, d, nd, ctypes.byref(out)))
+    return {int(k): v for k, v in json.loads(take_string(out)).items()}

@@ -106,3 +106,30 @@ def test_live_random_sweep_against_reference():
     assert len(outs) == len(cmds)
     bad = [(c, o) for c, o in zip(cmds, outs) if _canon_error(run(c)) != _canon_error(o)]
     assert not bad, bad[:3]
+
+
+def test_volume_report_matches_reference():
+    """volume_report (reference bsr.hpp:107-108, bsr.cpp:244-261) over fused
+    switch plans: the C ABI (hs_volume_report) and the CLI's JSON form
+    (formats.volume_report) against the reference's own output recorded by
+    ref_tool R (tests/golden/volume.jsonl, make_volume_golden.py)."""
+    import json as _json
+    from paper_2504_20490_b200 import formats as F
+    from paper_2504_20490_b200 import hshard as H
+    path = os.path.join(os.path.dirname(__file__), "golden", "volume.jsonl")
+    cases = [_json.loads(l) for l in open(path)]
+    assert len(cases) >= 40
+    for c in cases:
+        node_of = {int(k): v for k, v in c["node_of"].items()}
+        ents = [(tid, src, dst, tuple(shape)) for tid, eb, shape, src, dst in c["entries"]]
+        want = c["out"]
+        try:
+            plan = H.plan_switch(ents, {2: "bf16", 4: "f32", 8: "f64"}[c["entries"][0][1]])
+            got = H.volume_report(plan, node_of)
+        except H.HshardError as e:
+            assert "error" in want and e.code == want["error"], (c["name"], e)
+            continue
+        assert "error" not in want, c["name"]
+        assert {str(k): v for k, v in got.items()} == want, c["name"]
+        js = F.volume_report(_json.loads(plan.dump())["xfer"], node_of=node_of)
+        assert {str(k): v for k, v in js.items()} == want, c["name"]
