@@ -127,7 +127,9 @@ def main():
             ok = ok and bool(torch.equal(dst[i].float(), want))
         okt = torch.tensor([1.0 if ok else 0.0], device="cuda")
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        dst_bytes = sum(x.numel() for x in dst) * 2 * world
+        db = torch.tensor([float(sum(x.numel() for x in dst) * 2)], device="cuda")
+        dist.all_reduce(db, op=dist.ReduceOp.SUM)  # destination-resident bytes, all ranks
+        dst_bytes = db.item()
         if rank == 0:
             print(json.dumps({"workload": name, "n_gpus": world, "transport": "nccl collectives (torch.distributed)",
                               "ms": ms.item(), "GB/s": dst_bytes / (ms.item() * 1e-3) / 1e9,
