@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <numeric>
 #include <set>
 #include <sstream>
@@ -53,6 +54,26 @@ constexpr int kSlots = 9;
 // HS_PROG_BULK_STORE: a copy's outputs stored by TMA bulk stores (the rest from
 // registers, so the TMA unit still has room for the loads feeding the stages)
 constexpr int kBulkStoreOutputs = 2;
+
+// A task's inputs -- phase, tensor, (rank), box, terms, groups -- as raw words:
+// tasks with equal keys compute the same values (output merging, sharing).
+std::string input_key(const BoxTask& t, bool with_rank) {
+  std::string k;
+  k.reserve(64 + 16 * t.box.bounds.size() + 8 * (t.terms.size() + t.groups.size()));
+  auto put = [&k](int64_t v) { k.append(reinterpret_cast<const char*>(&v), sizeof v); };
+  put(t.phase);
+  put(t.tensor);
+  put(with_rank ? t.rank : -1);
+  put(static_cast<int64_t>(t.box.bounds.size()));
+  for (const auto& b : t.box.bounds) {
+    put(b[0]);
+    put(b[1]);
+  }
+  put(static_cast<int64_t>(t.terms.size()));
+  for (const Operand& o : t.terms) put((static_cast<int64_t>(o.state) << 32) | static_cast<uint32_t>(o.dev));
+  for (int g : t.groups) put(g);
+  return k;
+}
 
 SliceRegion bounds_only(const SliceRegion& r) {
   SliceRegion b;
@@ -360,6 +381,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     if (const char* e = std::getenv("HS_CE_CHUNKS")) ce_chunks_ = std::max(1, std::atoi(e));
   }
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
+  clock_.mark("rewrites:replicas");
   const bool two_phase = mid_state_ >= 0 && n_phases_ == 2 && !(flags_ & HS_PROG_NO_FUSE);
   auto rank_of = [this](const Operand& o, int t) { return loc(o.state, t, o.dev).rank; };
   // Cross-rank rewrites (world > 1), each behind a flag because which wins
@@ -370,6 +392,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   //               to several outputs (moves work off busy receivers).
   auto finish = [&](std::vector<BoxTask> ts) {
     if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_SHARE)) ts = spread_shared(std::move(ts));
+    clock_.mark("rewrites:share");
     if (ctx_.world() > 1 && (flags_ & HS_PROG_PUSH_ALL))
       for (BoxTask& t : ts)
         if (t.terms.size() == 1) {
@@ -571,8 +594,12 @@ void Program::choose_replicas(std::vector<BoxTask>& tasks) {
       if (cur.rank == t.rank) continue;
       DeviceId best = o.dev;
       int best_rank = cur.rank;
-      for (const auto& [key, L] : states_[o.state]) {
-        if (key.first != t.tensor || key.second == o.dev) continue;
+      // the state's shards of this tensor only (keys are ordered (tensor, device))
+      const auto& st = states_[o.state];
+      for (auto it = st.lower_bound({t.tensor, std::numeric_limits<DeviceId>::min()});
+           it != st.end() && it->first.first == t.tensor; ++it) {
+        const auto& [key, L] = *it;
+        if (key.second == o.dev) continue;
         const bool same = L.region.covers(t.box) &&
                           L.region.partial_index == cur.region.partial_index &&
                           L.region.partial_count == cur.region.partial_count &&
@@ -931,19 +958,13 @@ double Program::estimate_seconds(const std::vector<BoxTask>& tasks, int phases) 
 // chunk once and stores it to every output (local or over NVLink).  A
 // reduce-scatter + all-gather, with the inputs of each chunk read once.
 std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
-  std::map<std::string, std::vector<int>> same;
+  std::unordered_map<std::string, std::vector<int>> same;
   std::vector<std::string> order;
+  same.reserve(tasks.size() * 2);
   for (int i = 0; i < static_cast<int>(tasks.size()); ++i) {
-    const BoxTask& t = tasks[i];
-    std::ostringstream k;
-    k << t.phase << '|' << t.tensor << '|';
-    for (const auto& b : t.box.bounds) k << b[0] << ',' << b[1] << ';';
-    k << '|';
-    for (const Operand& o : t.terms) k << o.state << ':' << o.dev << ',';
-    k << '|';
-    for (int g : t.groups) k << g << ',';
-    auto [it, fresh] = same.try_emplace(k.str());
-    if (fresh) order.push_back(k.str());
+    std::string k = input_key(tasks[i], false);
+    auto [it, fresh] = same.try_emplace(k);
+    if (fresh) order.push_back(std::move(k));
     it->second.push_back(i);
   }
   std::vector<BoxTask> out;
@@ -983,26 +1004,12 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
 
 // ---------------------------------------------------------------- output merging
 std::vector<BoxTask> Program::merge_outputs(std::vector<BoxTask> tasks) {
-  // key: the task's inputs (phase, tensor, rank, box, terms, groups) as raw words
   std::unordered_map<std::string, int> index;
   index.reserve(tasks.size() * 2);
   std::vector<BoxTask> out;
   out.reserve(tasks.size());
-  std::string k;
-  auto put = [&k](int64_t v) { k.append(reinterpret_cast<const char*>(&v), sizeof v); };
   for (BoxTask& t : tasks) {
-    k.clear();
-    put(t.phase);
-    put(t.tensor);
-    put(t.rank);
-    put(static_cast<int64_t>(t.box.bounds.size()));
-    for (const auto& b : t.box.bounds) {
-      put(b[0]);
-      put(b[1]);
-    }
-    put(static_cast<int64_t>(t.terms.size()));
-    for (const Operand& o : t.terms) put((static_cast<int64_t>(o.state) << 32) | static_cast<uint32_t>(o.dev));
-    for (int g : t.groups) put(g);
+    const std::string k = input_key(t, true);
     auto it = index.find(k);
     if (it != index.end() && out[it->second].dsts.size() < static_cast<size_t>(kMaxOuts)) {
       BoxTask& m = out[it->second];
