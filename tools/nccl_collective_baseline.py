@@ -79,11 +79,24 @@ def main():
                    for d in mine]
             rank_rows = [(rows[r * per][0], rows[(r + 1) * per - 1][1]) for r in range(world)]
 
-        def step():
+        def pre_reduce():
             acc.copy_(src[0])  # local pre-reduction, ascending device id, fp32, one rounding
             for x in src[1:]:
                 acc.add_(x)
             s16.copy_(acc)
+
+        def collective():
+            if name == "cfg2d":
+                dist.reduce_scatter_tensor(recv, packed.view(world, -1), op=dist.ReduceOp.SUM)
+            elif name == "cfg3a":
+                dist.all_reduce(s16, op=dist.ReduceOp.SUM)
+            else:
+                for r in range(world):
+                    lo, hi = rank_rows[r]
+                    dist.reduce(s16[lo:hi], dst=r, op=dist.ReduceOp.SUM)
+
+        def step():
+            pre_reduce()
             if name == "cfg2d":
                 packed.copy_(s16.view(shape[0], world, per, cols).permute(1, 2, 0, 3))
                 dist.reduce_scatter_tensor(recv, packed.view(world, -1), op=dist.ReduceOp.SUM)
@@ -112,6 +125,18 @@ def main():
         ev1.synchronize()
         ms = torch.tensor([ev0.elapsed_time(ev1) / a.steps], device="cuda")
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        # the NCCL collective alone (same buffers, no local pre-reduction / copies)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record()
+        for _ in range(a.steps):
+            collective()
+        ev1.record()
+        ev1.synchronize()
+        coll = torch.tensor([ev0.elapsed_time(ev1) / a.steps], device="cuda")
+        dist.all_reduce(coll, op=dist.ReduceOp.MAX)
+        step()  # restore a correct result for the check below
+        torch.cuda.synchronize()
         # exactness on the integer grid: every destination box equals the logical sum
         full = torch.zeros(shape, dtype=torch.float32, device="cuda")
         for d in range(V):
@@ -132,7 +157,8 @@ def main():
         dst_bytes = db.item()
         if rank == 0:
             print(json.dumps({"workload": name, "n_gpus": world, "transport": "nccl collectives (torch.distributed)",
-                              "ms": ms.item(), "GB/s": dst_bytes / (ms.item() * 1e-3) / 1e9,
+                              "ms": ms.item(), "collective_only_ms": coll.item(),
+                              "GB/s": dst_bytes / (ms.item() * 1e-3) / 1e9,
                               "verified_exact_grid": okt.item() == 1.0, "nccl": torch.cuda.nccl.version()}),
                   flush=True)
         del src, acc, s16, dst, full
