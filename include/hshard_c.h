@@ -175,9 +175,12 @@ enum {
   HS_PROG_SMALL_ITEMS = 1 << 27,  /* 16 KB TMA work items instead of 32 KB: plan-dependent (faster
                                      for two-output copies, slower for long single-output ones) --
                                      the autotuner times it */
-  HS_PROG_NO_PDL = 1 << 28        /* launch phase kernels without programmatic dependent launch
+  HS_PROG_NO_PDL = 1 << 28,       /* launch phase kernels without programmatic dependent launch
                                      (default: each launch is scheduled while the previous one on
                                      the stream drains and waits for it on the device) */
+  HS_PROG_INTERLEAVE = 1 << 29    /* world > 1, unstreamed launches: items of tasks with NVLink
+                                     operands and of local-only tasks are merged evenly in launch
+                                     order (default: task order) -- the autotuner times it */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

@@ -625,14 +625,24 @@ __device__ __forceinline__ uint4 tma_record(const PhaseTables& t, int i, int lan
 
 // Expands a launch's records from its task descriptors on the device, one
 // warp per item (grid-stride): what the host used to build item by item.
+// `na` in (0, n_items): items [0, na) (tasks with NVLink operands) and
+// [na, n_items) (local-only tasks) are interleaved evenly in launch order --
+// the k-th of the first class goes to slot ceil((k+1) n / na) - 1, the k-th of
+// the second to floor(k n / (n - na)), a partition of [0, n) -- so the CTAs
+// keep NVLink and HBM busy together instead of one class after the other.
 template <int kEs>
-__global__ void __launch_bounds__(256) expand_records_kernel(PhaseTables t, uint4* recs, int W) {
+__global__ void __launch_bounds__(256) expand_records_kernel(PhaseTables t, uint4* recs, int W, int na) {
   const int lane = threadIdx.x & 31;
   const int warps = static_cast<int>(gridDim.x * blockDim.x) >> 5;
+  const int64_t n = t.n_items;
   int cur = 0;
   for (int i = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < t.n_items; i += warps) {
     const uint4 w = tma_record<kEs>(t, i, lane, cur);
-    if (lane < W) recs[static_cast<size_t>(i) * W + lane] = w;
+    int64_t slot = i;
+    if (na > 0 && na < n)
+      slot = i < na ? ((static_cast<int64_t>(i) + 1) * n + na - 1) / na - 1
+                    : ((static_cast<int64_t>(i) - na) * n) / (n - na);
+    if (lane < W) recs[static_cast<size_t>(slot) * W + lane] = w;
   }
 }
 
@@ -1398,13 +1408,13 @@ struct VerifyK {
 int tma_grid(int sm_count) { return sm_count; }
 
 cudaError_t launch_expand_records(const PhaseTables& t, int dtype, uint4* recs, int rec_words, int sm_count,
-                                  cudaStream_t s) {
+                                  int interleave, cudaStream_t s) {
   if (t.n_items == 0) return cudaSuccess;
   const int blocks = std::max(1, std::min(sm_count * 8, (t.n_items + 7) / 8));
   switch (dtype) {
-    case 0: case 2: expand_records_kernel<4><<<blocks, 256, 0, s>>>(t, recs, rec_words); break;
-    case 1: case 3: expand_records_kernel<8><<<blocks, 256, 0, s>>>(t, recs, rec_words); break;
-    case 4: expand_records_kernel<2><<<blocks, 256, 0, s>>>(t, recs, rec_words); break;
+    case 0: case 2: expand_records_kernel<4><<<blocks, 256, 0, s>>>(t, recs, rec_words, interleave); break;
+    case 1: case 3: expand_records_kernel<8><<<blocks, 256, 0, s>>>(t, recs, rec_words, interleave); break;
+    case 4: expand_records_kernel<2><<<blocks, 256, 0, s>>>(t, recs, rec_words, interleave); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

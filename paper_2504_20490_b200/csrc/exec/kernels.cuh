@@ -152,9 +152,10 @@ cudaError_t launch_phase(const PhaseTables& t, int dtype, int vec_bytes, bool tm
                          int grid, cudaStream_t s);
 int tma_grid(int sm_count);
 // Writes the launch's TMA item records (t.recs, t.rec_words words each) from
-// its task descriptors (t.ttasks), on the device.
+// its task descriptors (t.ttasks), on the device.  interleave in (0, n_items):
+// the first `interleave` items and the rest are merged evenly in launch order.
 cudaError_t launch_expand_records(const PhaseTables& t, int dtype, uint4* recs, int rec_words, int sm_count,
-                                  cudaStream_t s);
+                                  int interleave, cudaStream_t s);
 
 // Counter-hash payload generator (mirror of oracle/datagen.py).
 struct FillDesc {

@@ -1555,6 +1555,26 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
   }
 
   clock_.mark("queues");
+  // HS_PROG_INTERLEAVE (unstreamed multi-GPU launches): tasks with NVLink
+  // operands first, then local-only tasks; the record expansion merges the two
+  // item ranges evenly in launch order.
+  std::vector<int> interleave(n_phases_, 0);
+  if (ctx_.world() > 1 && !streamed_ && (flags_ & HS_PROG_INTERLEAVE))
+    for (int p = 0; p < n_phases_; ++p) {
+      Host& H = ph[p];
+      auto remote = [&](const TmaGeom& g) {
+        const BoxTask& bt = *H.src[g.task];
+        for (const auto* ops : {&bt.dsts, &bt.terms})
+          for (const Operand& o : *ops)
+            if (loc(o.state, bt.tensor, o.dev).rank != bt.rank) return true;
+        return false;
+      };
+      std::stable_partition(H.tma.begin(), H.tma.end(), remote);
+      int64_t na = 0;
+      for (const TmaGeom& g : H.tma) na += remote(g) ? g.count : 0;
+      interleave[p] = static_cast<int>(na);
+    }
+
   // TMA task descriptors in item order (+ a sentinel whose item0 is the item
   // count); the producer warp decodes every item's record from them.
   std::vector<std::vector<TmaTask>> ttasks(n_phases_);
@@ -1677,7 +1697,7 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       }
       if (l.tma && !ctx_.is_analysis())
         cuda_check(launch_expand_records(l.tables, dtype_, const_cast<uint4*>(l.tables.recs), l.tables.rec_words,
-                                         ctx_.sm_count(), ctx_.stream()),
+                                         ctx_.sm_count(), interleave[p], ctx_.stream()),
                    "expand records");
       if (l.tma) {
         stats_.tma_items += cnt;

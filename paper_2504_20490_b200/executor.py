@@ -48,6 +48,7 @@ HS_PROG_BULK_STORE = 1 << 25  # static TMA kernel: copies' first two outputs lea
 HS_PROG_SEPARATE_BARRIERS = 1 << 26  # world > 1: barriers as their own launches, not kernel prologues
 HS_PROG_SMALL_ITEMS = 1 << 27  # 16 KB TMA work items (plan-dependent; autotuned at N=1)
 HS_PROG_NO_PDL = 1 << 28  # no programmatic dependent launch between phase kernels (A/B)
+HS_PROG_INTERLEAVE = 1 << 29  # world > 1: NVLink and local-only items merged evenly in launch order
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,
@@ -580,7 +581,12 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_BULK_STORE,
                        # relays pushed while local groups reduce, then a short consume phase
                        HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM,
-                       HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_NO_SHARE]
+                       HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_NO_SHARE,
+                       # NVLink and local-only items merged evenly in launch order
+                       HS_PROG_INTERLEAVE, HS_PROG_INTERLEAVE | HS_PROG_NO_SHARE | HS_PROG_BULK_STORE,
+                       HS_PROG_INTERLEAVE | HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM,
+                       HS_PROG_INTERLEAVE | HS_PROG_NO_STREAM,
+                       HS_PROG_INTERLEAVE | HS_PROG_PULL_MID | HS_PROG_NO_STREAM]
 AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE, HS_PROG_SMALL_ITEMS, HS_PROG_SMALL_ITEMS | HS_PROG_BULK_STORE]
 TUNE_MARGIN = 0.01  # a later candidate must beat the best so far by 1% (timing noise)
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every
@@ -626,6 +632,7 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
             continue
         two_phase_only = (HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_PULL_MID | HS_PROG_STREAM_SHARE(0xFF)
                           | HS_PROG_FUSE_PHASES | HS_PROG_CE_RELAY)
+        # (HS_PROG_INTERLEAVE alone applies to single-phase plans too)
         if flags & two_phase_only and prog.stats()["plan_phases"] < 2:  # same program as another candidate
             prog.close()
             continue

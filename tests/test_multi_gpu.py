@@ -37,6 +37,8 @@ def _gpus():
                                    "67108864,67121152",
                                    # TMA bulk stores (to peers when pushed): alone, NO_SHARE, fan-out once
                                    "33554432,33554560,33587200",
+                                   # NVLink / local items interleaved: alone, keep-local relays, pull-mid
+                                   "536870912,536875520,536883200",
                                    # BASELINE reduction configs at FULL size, real-valued payloads,
                                    # vs the native CPU executor: default, plain, pull-mid, fused
                                    "full:0,14,12288,1"])
