@@ -1689,7 +1689,11 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
       l.tables.first_ctas = l.grid;
       l.tables.error = ctx_.error_flag();
       l.tables.bulk_store = (flags_ & HS_PROG_BULK_STORE) ? kBulkStoreOutputs : 0;
-      l.tables.pdl = !(flags_ & HS_PROG_NO_PDL) && !ce_mode_;
+      // Programmatic dependent launch on one GPU only: at N > 1 the launches
+      // open with cross-rank barriers and gain little; an autotune sweep at N=2
+      // once failed with a launch error that did not reproduce, so the
+      // multi-rank path keeps plain stream order.
+      l.tables.pdl = !(flags_ & HS_PROG_NO_PDL) && ctx_.world() == 1;
       if (l.tma && std::getenv("HS_TRACE") && !ctx_.is_analysis()) {
         stats_.trace_off = ctx_.alloc(static_cast<size_t>(l.grid) * 64);
         stats_.trace_ctas = l.grid;
