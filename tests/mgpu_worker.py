@@ -159,12 +159,58 @@ def main():
         results.append({"case": "host-path", "flags": 0, "bad": bad, "nvlink_in": 0, "nvlink_out": 0})
         return not bad
 
+    def pointer_case():
+        """hs_prog_compile_ptrs at N > 1: every rank's shards are its own torch tensors;
+        peers' buffers are mapped through hs_ipc_export / hs_ipc_import
+        (executor.exchange_pointers); results bit-exact vs the oracle."""
+        from paper_2504_20490_b200.executor import PointerLayout, block_map, exchange_pointers
+        bad = []
+        for wname, shape in [("cfg2e", (128, 512)), ("cfg1C", (256, 64)), ("cfg3a", (64, 256))]:
+            w = W.by_name(wname)
+            _, src, dst, _ = w.transitions[0]
+            plan = H.classify(src, dst, shape, w.dtype)
+            vmap = block_map(w.n_virtual, world)
+            ref = ox.scatter(src, shape, w.dtype, 31, 0, "real")
+            want = ox.execute_plan(plan.json(), ref, w.dtype)
+            tdt = {"bf16": torch.int16, "f32": torch.float32}[w.dtype]
+            keep, mine = [], {}
+            for d, a in ref.items():
+                if vmap[d] == rank:
+                    t = torch.from_numpy(a.view(np.int16) if w.dtype == "bf16" else a).to(f"cuda:{local}")
+                    keep.append(t)
+                    mine[("src", 0, d)] = t.data_ptr()
+            outs = {}
+            for d, a in want.items():
+                if vmap[d] == rank:
+                    t = torch.zeros(a.shape, dtype=tdt, device=f"cuda:{local}")
+                    keep.append(t)
+                    outs[d] = t
+                    mine[("dst", 0, d)] = t.data_ptr()
+            torch.cuda.synchronize()
+            ptrs = exchange_pointers(ctx, mine)
+            lay = PointerLayout(w.n_virtual, 1, {(sl, d): p for (k, sl, d), p in ptrs.items() if k == "src"},
+                                {(sl, d): p for (k, sl, d), p in ptrs.items() if k == "dst"}, vmap)
+            prog = Program(ctx, plan, lay)
+            prog.run(torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            ctx.sync()
+            for d, t in outs.items():
+                if not np.array_equal(t.cpu().numpy().view(np.uint8), want[d].view(np.uint8)):
+                    bad.append((wname, d))
+            dist.barrier()  # peers finished reading my buffers before they go
+            prog.close()
+            del keep, outs
+        results.append({"case": "pointers", "flags": 0, "bad": bad, "nvlink_in": 0, "nvlink_out": 0})
+        return not bad
+
     lay_holder = []
     try:
         if full:
             full_size_cases()
             raise StopIteration
         if not host_path_case():
+            ok = False
+        if not pointer_case():
             ok = False
         for wname, shape in [("cfg1A", (256, 64)), ("cfg1B", (256, 64)), ("cfg1D", (256, 64)),
                              ("cfg2e", (64, 256)), ("cfg2b", (64, 256)), ("cfg3b", (64, 512)),
