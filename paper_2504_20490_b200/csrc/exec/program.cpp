@@ -519,6 +519,22 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
         remote_final_writes_ = remote_final_writes_ ||
                                (o.state == static_cast<int>(final_state_) && rank_of(o, t.tensor) != t.rank);
 
+  // The host-buffer path copies in only the source shards some task (on any
+  // rank) reads: replicas the program never sources from (replica choice,
+  // fusion) stay on the host -- cfg2e reads 6 of its 8 partials.
+  {
+    std::set<std::pair<int, DeviceId>> read;
+    for (const BoxTask& t : tasks)
+      for (const Operand& o : t.terms)
+        if (o.state == 0) read.insert({t.tensor, o.dev});
+    std::vector<std::tuple<DeviceId, int, char*, size_t>> kept;
+    for (const auto& h : host_src_)
+      if (read.count({std::get<1>(h), std::get<0>(h)})) kept.push_back(h);
+    stats_.h2d_bytes = 0;
+    for (const auto& h : kept) stats_.h2d_bytes += static_cast<int64_t>(std::get<3>(h));
+    host_src_ = std::move(kept);
+  }
+
   // ---- algorithmic byte accounting over ALL ranks' tasks, then keep ours
   const int me = ctx_.rank();
   std::vector<BoxTask> mine;
@@ -1952,6 +1968,7 @@ std::string Program::stats_json() const {
     << ",\"hbm_read\":" << stats_.hbm_read << ",\"hbm_write\":" << stats_.hbm_write
     << ",\"nvlink_in\":" << stats_.nvlink_in << ",\"nvlink_out\":" << stats_.nvlink_out
     << ",\"dst_bytes\":" << stats_.dst_bytes << ",\"src_bytes\":" << stats_.src_bytes
+    << ",\"h2d_bytes\":" << stats_.h2d_bytes
     << ",\"kernels_per_run\":" << stats_.kernels_per_run << ",\"streamed\":" << (stats_.streamed ? 1 : 0)
     << ",\"ce_relay\":" << (stats_.ce_relay ? 1 : 0) << ",\"ce_copies\":" << ce_copies_.size()
     << ",\"trace_off\":" << stats_.trace_off << ",\"trace_ctas\":" << stats_.trace_ctas

@@ -188,6 +188,7 @@ struct ProgramStats {
   int64_t nvlink_out = 0;    // bytes peers pull from this GPU
   int64_t dst_bytes = 0;     // destination-resident bytes on this rank
   int64_t src_bytes = 0;     // source-resident bytes on this rank
+  int64_t h2d_bytes = 0;     // host-buffer path: source bytes copied in per run (shards some task reads)
   int kernels_per_run = 0;   // phase kernels + barrier kernels
   bool streamed = false;     // both plan phases in one launch (ready flags)
   bool ce_relay = false;     // relays moved by the copy engines
