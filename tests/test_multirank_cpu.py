@@ -201,3 +201,23 @@ dist.destroy_process_group()
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert res.returncode == 0, res.stderr[-4000:]
     assert out.read_text() == "ok"
+
+
+def test_interleave_slots_partition():
+    """HS_PROG_INTERLEAVE's launch order (kernels.cu expand_records_kernel): the
+    k-th item of the NVLink class goes to slot ceil((k+1) n / na) - 1, the k-th
+    local item to floor(k n / (n - na)); together a permutation of [0, n) that
+    spreads the classes evenly (every prefix holds its share of each class)."""
+    for n in range(1, 400):
+        for na in range(1, n):
+            a = [((k + 1) * n + na - 1) // na - 1 for k in range(na)]
+            b = [(k * (n)) // (n - na) for k in range(n - na)]
+            assert sorted(a + b) == list(range(n)), (n, na)
+            # evenness: within any prefix of j slots, the NVLink-class count is within 1 of j*na/n
+            is_a = [0] * n
+            for x in a:
+                is_a[x] = 1
+            c = 0
+            for j in range(n):
+                c += is_a[j]
+                assert abs(c - (j + 1) * na / n) <= 1.0 + 1e-9, (n, na, j)
