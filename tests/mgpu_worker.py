@@ -203,8 +203,42 @@ def main():
         results.append({"case": "pointers", "flags": 0, "bad": bad, "nvlink_in": 0, "nvlink_out": 0})
         return not bad
 
+    def random_cases():
+        """Random plans of every step kind and dtype (tests/golden/gen_cases.rand_pair,
+        the same seeded list on every rank), 10 virtual devices block-mapped onto the
+        ranks, each through every flag set, bit-exact vs the oracle on each rank."""
+        import random as _random
+
+        from gen_cases import rand_pair, zero_width
+        rng = _random.Random(2026)
+        dtypes = ["bf16", "f32", "f64", "i32", "i64"]
+        done = 0
+        tries = 0
+        while done < int(os.environ.get("HS_MGPU_RANDOM_N", "60")) and tries < 5000:
+            tries += 1
+            src, dst, shape = rand_pair(rng)
+            dtype = dtypes[tries % len(dtypes)]
+            if zero_width(src, shape) or zero_width(dst, shape):
+                continue
+            try:
+                plan = H.classify(src, dst, shape, dtype)
+                ox.execute_plan(plan.json(), ox.scatter(src, shape, dtype, 11, 0, "grid"), dtype)
+            except (H.HshardError, ox.OracleError):
+                continue
+            mode = "real" if dtype in ("bf16", "f32", "f64") else "grid"
+
+            def src_of(src=src, shape=shape, dtype=dtype, plan=plan, mode=mode):
+                s_ = ox.scatter(src, shape, dtype, 11, 0, mode)
+                out = ox.execute_plan(plan.json(), s_, dtype)
+                return {(0, d): a for d, a in out.items()}
+            run_case(f"rand{done}", plan, 10, src_of, dtype, mode)
+            done += 1
+
     lay_holder = []
     try:
+        if os.environ.get("HS_MGPU_RANDOM") == "1":
+            random_cases()
+            raise StopIteration
         if full:
             full_size_cases()
             raise StopIteration

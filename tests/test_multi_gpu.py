@@ -39,6 +39,8 @@ def _gpus():
                                    "33554432,33554560,33587200",
                                    # NVLink / local items interleaved: alone, keep-local relays, pull-mid
                                    "536870912,536875520,536883200",
+                                   # 60 random plans of every kind and dtype through several variants
+                                   "random:0,14,1,12288,536870912",
                                    # BASELINE reduction configs at FULL size, real-valued payloads,
                                    # vs the native CPU executor: default, plain, pull-mid, fused
                                    "full:0,14,12288,1"])
@@ -54,6 +56,8 @@ def test_multi_gpu_parity(tmp_path, flags):
         env["HS_STREAM_CHUNK_KB"] = "1"
     if flags.startswith("full:"):
         env["HS_MGPU_FULL"] = "1"
+    if flags.startswith("random:"):
+        env["HS_MGPU_RANDOM"] = "1"
     if flags.startswith("ce3:"):  # copy-engine relays in 3 chunks (uneven row cuts)
         env["HS_CE_CHUNKS"] = "3"
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800, cwd=ROOT, env=env)
