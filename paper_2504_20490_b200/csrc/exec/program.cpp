@@ -984,8 +984,9 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
     it->second.push_back(i);
   }
   std::vector<BoxTask> out;
+  out.reserve(tasks.size());
   for (const std::string& key : order) {
-    const std::vector<int>& idx = same[key];
+    const std::vector<int>& idx = same.find(key)->second;
     std::set<int> ranks;
     std::vector<Operand> dsts;
     for (int i : idx) {
@@ -999,7 +1000,7 @@ std::vector<BoxTask> Program::spread_shared(std::vector<BoxTask> tasks) {
       if (T.box.bounds[d][1] - T.box.bounds[d][0] >= static_cast<int64_t>(ranks.size())) split = static_cast<int>(d);
     const bool worth = ranks.size() >= 2 && split >= 0;
     if (!worth || dsts.size() > static_cast<size_t>(kMaxOuts) || T.terms.empty()) {
-      for (int i : idx) out.push_back(tasks[i]);
+      for (int i : idx) out.push_back(std::move(tasks[i]));
       continue;
     }
     const int64_t lo = T.box.bounds[split][0], ext = T.box.bounds[split][1] - lo;

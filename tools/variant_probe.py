@@ -61,10 +61,22 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.all_reduce(bad, op=dist.ReduceOp.MAX)
         st = prog.stats()
+        prog.profile(True)  # separate pass: per-phase durations on every rank
+        for _ in range(20):
+            prog.run(stream.cuda_stream)
+        stream.synchronize()
+        ctx.sync()
+        ph, runs = prog.phase_ms()
+        mine = {"rank": rank, "phase_ms": [x / max(1, runs) for x in ph], "phase_bytes": st["phase_bytes"],
+                "kernels": st["phase_kernels"]}
+        per = [mine]
+        if world > 1:
+            per = [None] * world
+            dist.all_gather_object(per, mine)
         if rank == 0:
             print(json.dumps({"workload": a.workload, "n": world, "flags": f, "ms": t.item(),
                               "verified": bad.item() == 0, "streamed": st["streamed"],
-                              "phases": st["phases"]}), flush=True)
+                              "phases": st["phases"], "ranks": per}), flush=True)
         prog.close()
         if world > 1:
             dist.barrier()
