@@ -57,6 +57,9 @@ def parse():
                     help="comma list of workloads (or 'all'): one JSON line per workload instead "
                          "of the headline line")
     ap.add_argument("--no-tune", action="store_true", help="no autotuning of the program variant")
+    ap.add_argument("--cpu-sweep", default=None,
+                    help="comma list of workloads (or 'all'): the CPU baselines only (BASELINE.md §3), "
+                         "one JSON line per workload; no GPU needed")
     ap.add_argument("--flags", type=int, default=0,
                     help="HS_PROG_* bits: 1 fuse, 2 no-fuse, 4 no-TMA, 8 no-merge (14 = plain baseline)")
     return ap.parse_args()
@@ -224,6 +227,60 @@ def native_run(w, reps: int, warmup: int, threads: int) -> dict:
     return j
 
 
+def native_switch_run(entries, dtype: str, reps: int, warmup: int, threads: int) -> dict:
+    """oracle/_ref/ref_tool W: build_table per parameter + fuse (reference planner), then
+    every local copy and transfer as row memcpys over host threads (native dtype)."""
+    cmd = f"W|{dtype}|u|{len(entries)}|1|{reps}|{threads}|{warmup}\n"
+    for tid, s_, d_, shp in entries:
+        cmd += f"{tid}|{','.join(map(str, shp))}|{s_}|{d_}\n"
+    return _ref_tool(cmd)
+
+
+def cpu_sweep(args):
+    """BASELINE.md §3 item 2 on every config: the CPU memcpy executor at all host threads and
+    at 1 thread (classify configs at full size; switch configs in parameter batches small
+    enough for host RAM, times summed over the batches), plus the reference-faithful form
+    (item 1) on a row sample of configs 1-3.  One JSON line per workload."""
+    from paper_2504_20490_b200 import workloads as W
+    nproc = os.cpu_count() or 1
+    names = [x.name for x in W.all_workloads()] if args.cpu_sweep == "all" else args.cpu_sweep.split(",")
+    for name in names:
+        w = W.by_name(name)
+        rec = {"workload": name, "dtype": w.dtype, "cpu_model": cpu_model(), "nproc": nproc}
+        if w.kind == "classify":
+            for threads, reps in ((nproc, 5), (1, 1)):
+                j = native_run(w, reps, 1 if threads > 1 else 0, threads)
+                rec[f"memcpy_{threads}t"] = {"ms": j["mean"] * 1e3, "GB/s": j["dst_bytes"] / j["mean"] / 1e9,
+                                             "best_ms": j["seconds"] * 1e3, "reps": j["reps"]}
+            r = reference_primitive_run(w, 1, 0, nproc, rows_cap=1024)
+            rec["reference_primitives_sample"] = {"rows": r["shape"][0], "ms": r["seconds"] * 1e3,
+                                                  "GB/s": r["dst_bytes"] / r["seconds"] / 1e9}
+        else:
+            # batches of parameters (~6 GB of source per batch) so host RAM suffices
+            es = DTYPE_BYTES[w.dtype]
+            batches, cur, cur_b = [], [], 0
+            for e in w.transitions:
+                n = 1
+                for x in e[3]:
+                    n *= x
+                cur.append(e)
+                cur_b += n * es
+                if cur_b > 6e9:
+                    batches.append(cur)
+                    cur, cur_b = [], 0
+            if cur:
+                batches.append(cur)
+            for threads in (nproc, 1):
+                tot_s, tot_b = 0.0, 0
+                for b in batches:
+                    j = native_switch_run(b, w.dtype, 1, 0, threads)
+                    tot_s += j["mean"]
+                    tot_b += j["dst_bytes"]
+                rec[f"memcpy_{threads}t"] = {"ms": tot_s * 1e3, "GB/s": tot_b / tot_s / 1e9,
+                                             "batches": len(batches)}
+        print(json.dumps(rec), flush=True)
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -376,6 +433,10 @@ def main():
     if args.impl == "reference":
         # rank 0 alone, no process group, no torch, no product library
         reference_arm(args, w, rank, world)
+        return
+    if args.cpu_sweep:
+        if rank == 0:
+            cpu_sweep(args)
         return
     if world > 1:
         import torch.distributed as dist
