@@ -221,3 +221,45 @@ def test_interleave_slots_partition():
             for j in range(n):
                 c += is_a[j]
                 assert abs(c - (j + 1) * na / n) <= 1.0 + 1e-9, (n, na, j)
+
+
+def test_state_layouts_chain_and_transition_offsets():
+    """executor.StateLayout packs one strategy's shards symmetrically (identical offsets
+    on every rank by construction, within the requested base); Transition indexes them
+    by the switch plan's tensor order, matched by tensor id -- a plan that lists only
+    some parameters, in its own order, still finds every shard."""
+    import numpy as np
+    from paper_2504_20490_b200 import hshard as H
+    from paper_2504_20490_b200 import workloads as W
+    from paper_2504_20490_b200.executor import SIZE_MAX, StateLayout, Transition, block_map
+
+    class Ctx:
+        def __init__(self, rank, world):
+            self.rank, self.world, self.arena_bytes = rank, world, 1 << 40
+
+        def alloc(self, n):
+            raise AssertionError("explicit bases only")
+
+    w = W.config4()
+    src = [(i, t, s, shp) for i, (t, s, d, shp) in enumerate(w.transitions)]
+    dst = [(i, t, d, shp) for i, (t, s, d, shp) in enumerate(w.transitions)]
+    for world in (1, 2, 4, 8):
+        size = StateLayout.bytes_needed(src, "bf16", 8, world)
+        lays = [StateLayout(Ctx(r, world), src, "bf16", 8, base=4096) for r in range(world)]
+        recs = [sorted((k, v["offset"], v["rank"], v["bytes"]) for k, v in l.recs.items()) for l in lays]
+        assert all(r == recs[0] for r in recs)                      # symmetric
+        assert max(o + b for _, o, _, b in recs[0]) <= 4096 + size  # within the reservation
+        vmap = block_map(8, world)
+        assert all(rank == vmap[k[1]] for k, _, rank, _ in recs[0])
+    # a plan over a reversed subset of the tensors: offsets follow tensor ids
+    sub = list(reversed(w.transitions[:5]))
+    plan = H.plan_switch(sub, "bf16")
+    a = StateLayout(Ctx(0, 1), src, "bf16", 8, base=0)
+    b = StateLayout(Ctx(0, 1), dst, "bf16", 8, base=1 << 36)
+    tr = Transition(plan, a, b)
+    offs = np.array(tr._offs[0])
+    for slot, (tid, s, d, shp) in enumerate(sub):
+        for dev in range(8):
+            rec = next((v for (sl, dv), v in a.recs.items() if v["tid"] == tid and dv == dev), None)
+            want = rec["offset"] if rec else SIZE_MAX
+            assert offs[slot * 8 + dev] == want, (tid, dev)
