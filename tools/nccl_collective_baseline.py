@@ -47,6 +47,9 @@ def main():
     ap.add_argument("--configs", default="cfg2d,cfg3a,cfg3b")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--hierarchical", action="store_true",
+                    help="cfg3a lowered literally on NCCL sub-communicators (N=4): AllReduce within each "
+                         "subgroup's GPUs, then between the subgroups' GPU pairs (i, i + N/2)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -55,6 +58,14 @@ def main():
     V = 8
     per = V // world
     mine = list(range(rank * per, (rank + 1) * per))
+    sub_groups = pair_groups = None
+    if a.hierarchical:
+        half = world // 2
+        # every rank creates every group (torch.distributed requirement); NCCL splits them
+        sub = [dist.new_group(list(range(0, half))), dist.new_group(list(range(half, world)))]
+        pairs = [dist.new_group([i, i + half]) for i in range(half)]
+        sub_groups = sub[rank // half]
+        pair_groups = pairs[rank % half]
     for name in a.configs.split(","):
         if name == "cfg2d":
             shape = (8192, 8192)
@@ -88,6 +99,11 @@ def main():
         def collective():
             if name == "cfg2d":
                 dist.reduce_scatter_tensor(recv, packed.view(world, -1), op=dist.ReduceOp.SUM)
+            elif name == "cfg3a" and a.hierarchical:
+                # AR{0..3}, AR{4..7} on the subgroups' GPUs, then SplitAllReduce between the
+                # subgroups (c {0,4}), every receiver pair (i, i + N/2) at once
+                dist.all_reduce(s16, op=dist.ReduceOp.SUM, group=sub_groups)
+                dist.all_reduce(s16, op=dist.ReduceOp.SUM, group=pair_groups)
             elif name == "cfg3a":
                 dist.all_reduce(s16, op=dist.ReduceOp.SUM)
             else:
@@ -103,7 +119,7 @@ def main():
                 for i, d in enumerate(dst):
                     d.copy_(recv[i])
             elif name == "cfg3a":
-                dist.all_reduce(s16, op=dist.ReduceOp.SUM)
+                collective()
                 for d in dst:
                     d.copy_(s16)
             else:
@@ -156,7 +172,9 @@ def main():
         dist.all_reduce(db, op=dist.ReduceOp.SUM)  # destination-resident bytes, all ranks
         dst_bytes = db.item()
         if rank == 0:
-            print(json.dumps({"workload": name, "n_gpus": world, "transport": "nccl collectives (torch.distributed)",
+            print(json.dumps({"workload": name, "n_gpus": world,
+                              "transport": "nccl collectives (torch.distributed)" +
+                                           (", hierarchical sub-communicators" if a.hierarchical else ""),
                               "ms": ms.item(), "collective_only_ms": coll.item(),
                               "GB/s": dst_bytes / (ms.item() * 1e-3) / 1e9,
                               "verified_exact_grid": okt.item() == 1.0, "nccl": torch.cuda.nccl.version()}),
