@@ -417,6 +417,26 @@ def switch_latency(ctx, stream, steps, cycles, allreduce_max, barrier, warm_runs
                 rec["cold_over_warm"] = rec["cold_total_ms"] / rec["warm_ms"]
                 rec["tma_items"] = prog.stats()["tma_items"]
             out.append(rec)
+    # then each step's program variant is autotuned (untimed) and its warm time taken
+    # again: the cache now hands out the tuned program
+    for k, w in enumerate(steps):
+        tuned = cyc_obj.tune(k, stream, steps=3 if w.transitions and len(w.transitions) > 300 else 5)
+        prog, info = cyc_obj.prepare(k)
+        stream.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record()
+            for _ in range(warm_runs):
+                prog.run(sp)
+            b.record()
+        b.synchronize()
+        ctx.sync()
+        bad = cyc_obj.states[k + 1].verify(seed)
+        rec = out[(cycles - 1) * len(steps) + k]
+        rec["warm_tuned_ms"] = allreduce_max(a.elapsed_time(b) / warm_runs)
+        rec["tuned_flags"] = tuned["chosen_flags"]
+        rec["verified_tuned"] = bool(allreduce_max(float(bad)) == 0)
     sizes = cyc_obj.sizes
     cyc_obj.close()
     ctx.reset(0)

@@ -479,16 +479,34 @@ class StrategyCycle:
             base = 0 if k % 2 == 0 else (top - self.sizes[k]) // 256 * 256
             self.states.append(StateLayout(ctx, e, dtype, n_virtual, base=base))
         self.cache = SwitchCache(ctx)
+        self.step_flags: Dict[int, int] = {}  # per step: the variant tune() chose
 
     def prepare(self, k: int):
         """Plan (cached) and compile (cached) step k -> (program, info)."""
         t0 = time.perf_counter()
         plan, plan_hit = self.cache.plan(self.steps[k], self.dtype)
         t1 = time.perf_counter()
-        prog, prog_hit = self.cache.program(plan, self.states[k], self.states[k + 1], self.flags)
+        prog, prog_hit = self.cache.program(plan, self.states[k], self.states[k + 1],
+                                            self.step_flags.get(k, self.flags))
         t2 = time.perf_counter()
         return prog, {"plan_cached": plan_hit, "program_cached": prog_hit, "plan_ms": (t1 - t0) * 1e3,
-                      "compile_ms": (t2 - t1) * 1e3}
+                      "compile_ms": (t2 - t1) * 1e3, "flags": self.step_flags.get(k, self.flags)}
+
+    def tune(self, k: int, stream=None, steps: int = 5, group=None) -> dict:
+        """Autotune step k's program variant (executor.autotune, every rank together) and
+        keep the winner in the cache: later prepare(k) calls return it.  Rewrites the
+        destination state with the same values (the source state is only read)."""
+        plan, _ = self.cache.plan(self.steps[k], self.dtype)
+        prog, timings = autotune(self.ctx, plan, Transition(plan, self.states[k], self.states[k + 1]),
+                                 stream=stream, steps=steps, group=group)
+        key = (id(plan), self.states[k].base, self.states[k].size, self.states[k + 1].base,
+               self.states[k + 1].size, prog.flags)
+        old = self.cache.programs.get(key)
+        if old is not None and old is not prog:
+            old.close()
+        self.cache.programs[key] = prog
+        self.step_flags[k] = prog.flags
+        return {"chosen_flags": prog.flags, "ms_by_flags": timings}
 
     def close(self):
         self.cache.close()
