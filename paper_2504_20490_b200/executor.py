@@ -478,8 +478,20 @@ class StrategyCycle:
                 continue
             base = 0 if k % 2 == 0 else (top - self.sizes[k]) // 256 * 256
             self.states.append(StateLayout(ctx, e, dtype, n_virtual, base=base))
+        # Program scratch (intermediates, relays, ready flags) comes from the arena's
+        # bump allocator: start it past every low-placed state and keep it below every
+        # high-placed one, so no program's scratch overlaps a state.
+        self.scratch_lo = max(st.base + st.size for st in self.states if st.base == 0)
+        self.scratch_hi = min((st.base for st in self.states if st.base > 0), default=top)
+        if self.scratch_lo >= self.scratch_hi:
+            raise H.HshardError("ShapeMismatch", "no arena left between the layout states")
+        ctx.reset((self.scratch_lo + 255) // 256 * 256)
         self.cache = SwitchCache(ctx)
         self.step_flags: Dict[int, int] = {}  # per step: the variant tune() chose
+
+    def _check_scratch(self):
+        if self.ctx.alloc(0) > self.scratch_hi:
+            raise H.HshardError("ShapeMismatch", "program scratch reached a layout state")
 
     def prepare(self, k: int):
         """Plan (cached) and compile (cached) step k -> (program, info)."""
@@ -488,6 +500,7 @@ class StrategyCycle:
         t1 = time.perf_counter()
         prog, prog_hit = self.cache.program(plan, self.states[k], self.states[k + 1],
                                             self.step_flags.get(k, self.flags))
+        self._check_scratch()
         t2 = time.perf_counter()
         return prog, {"plan_cached": plan_hit, "program_cached": prog_hit, "plan_ms": (t1 - t0) * 1e3,
                       "compile_ms": (t2 - t1) * 1e3, "flags": self.step_flags.get(k, self.flags)}
@@ -499,6 +512,7 @@ class StrategyCycle:
         plan, _ = self.cache.plan(self.steps[k], self.dtype)
         prog, timings = autotune(self.ctx, plan, Transition(plan, self.states[k], self.states[k + 1]),
                                  stream=stream, steps=steps, group=group)
+        self._check_scratch()
         key = (id(plan), self.states[k].base, self.states[k].size, self.states[k + 1].base,
                self.states[k + 1].size, prog.flags)
         old = self.cache.programs.get(key)
