@@ -475,6 +475,11 @@ def main():
     arena = max(8 << 30, free - (10 << 30))
     if os.environ.get("HS_ARENA_GB"):
         arena = int(float(os.environ["HS_ARENA_GB"]) * (1 << 30))
+    if world > 1:  # the arena is symmetric: one size on every rank
+        import torch.distributed as dist
+        t_ = torch.tensor([float(arena)], dtype=torch.float64)
+        dist.all_reduce(t_, op=dist.ReduceOp.MIN)
+        arena = int(t_.item()) // (1 << 20) << 20
     ctx = Context(arena, rank=rank, world=world, gpu=local)
     if world > 1 and args.flags & 2048:
         ctx.init_nccl()

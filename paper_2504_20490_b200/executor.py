@@ -75,6 +75,7 @@ class Context:
         base, size = c_void_p(), c_size_t()
         check(LIB.hs_ctx_arena(self._h, ctypes.byref(base), ctypes.byref(size)))
         self.arena_base, self.arena_bytes = base.value, size.value
+        self.sym_bytes = self.arena_bytes  # min over ranks (set when the peers open)
         if world > 1:
             self._open_peers(group)
 
@@ -88,6 +89,11 @@ class Context:
         dist.all_gather(gathered, t, group=group)
         blob = b"".join(bytes(g.numpy().tobytes()) for g in gathered)
         check(LIB.hs_ctx_open_peers(self._h, blob))
+        # The arenas are symmetric only up to the smallest one: an offset is valid on
+        # every rank below it (layouts placed from the top must use it, not arena_bytes).
+        sz = torch.tensor([float(self.arena_bytes)], dtype=torch.float64)
+        dist.all_reduce(sz, op=dist.ReduceOp.MIN, group=group)
+        self.sym_bytes = int(sz.item())
 
     def init_nccl(self, group=None) -> None:
         """NCCL communicator over the same ranks (only the HS_PROG_NCCL baseline uses it)."""
@@ -321,7 +327,7 @@ class StateLayout:
         self.recs, used = self._pack(self.entries, self.es, self.n_virtual, self.v_to_rank, ctx.world)
         self.size = max(used) + 256
         self.base = ctx.alloc(self.size) if base is None else int(base)
-        if self.base + self.size > ctx.arena_bytes:
+        if self.base + self.size > getattr(ctx, "sym_bytes", ctx.arena_bytes):
             raise H.HshardError("ShapeMismatch", "state does not fit the arena")
         self._by_tid: Dict[int, Dict[int, int]] = {}
         for rec in self.recs.values():
@@ -465,7 +471,9 @@ class StrategyCycle:
         ents.append([(i, tid, d, shp) for i, (tid, s, d, shp) in enumerate(steps[-1])])
         closed = [e[1:] for e in ents[-1]] == [e[1:] for e in ents[0]]
         self.sizes = [StateLayout.bytes_needed(e, dtype, n_virtual, ctx.world) for e in ents]
-        top = ctx.arena_bytes // 256 * 256
+        # the top of the SYMMETRIC arena: every rank places the high states at the same
+        # offsets (arena sizes may differ between ranks)
+        top = getattr(ctx, "sym_bytes", ctx.arena_bytes) // 256 * 256
         need = max(self.sizes[k] + self.sizes[k + 1] for k in range(len(steps)))
         if need > top:
             raise H.HshardError("ShapeMismatch", f"two states need {need} bytes per GPU, arena {top}")
@@ -649,18 +657,23 @@ def autotune(ctx: Context, plan: H.Plan, layout: ShardLayout, stream=None, steps
     sp = s.cuda_stream
     best, best_ms, timings = None, None, {}
     for flags in cands:
+        mark = ctx.alloc(0)  # the arena cursor: scratch must stay symmetric across ranks
         try:
             prog = Program(ctx, plan, layout, flags)
         except H.HshardError:  # a variant this plan cannot take (e.g. a box shape a rewrite does not support)
             prog = None
         if ctx.world > 1:
-            # compile checks only see this rank's tasks: every rank skips together
+            # compile checks only see this rank's tasks: every rank skips together, and
+            # every rank rewinds the scratch the skipped variant allocated (a rank whose
+            # compile failed part-way allocated less), so later offsets stay symmetric
             ok = torch.tensor([0.0 if prog is None else 1.0], dtype=torch.float64)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
-            if ok.item() == 0.0 and prog is not None:
-                prog.close()
+            if ok.item() == 0.0:
+                if prog is not None:
+                    prog.close()
                 prog = None
         if prog is None:
+            ctx.reset(mark)
             continue
         two_phase_only = (HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM | HS_PROG_PULL_MID | HS_PROG_STREAM_SHARE(0xFF)
                           | HS_PROG_FUSE_PHASES | HS_PROG_CE_RELAY)

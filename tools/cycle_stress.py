@@ -31,7 +31,12 @@ def main():
     if world > 1:
         dist.init_process_group("gloo")
     free, _ = torch.cuda.mem_get_info(local)
-    ctx = Context(free - (12 << 30), rank=rank, world=world, gpu=local)
+    arena = free - (12 << 30)
+    if world > 1:  # one arena size on every rank (the arena is symmetric)
+        t_ = torch.tensor([float(arena)], dtype=torch.float64)
+        dist.all_reduce(t_, op=dist.ReduceOp.MIN)
+        arena = int(t_.item()) // (1 << 20) << 20
+    ctx = Context(arena, rank=rank, world=world, gpu=local)
     steps = ([W.config5(x) for x in W.CONFIG5_CYCLE] if a.workload == "cfg5"
              else [W.config4(), W.config4_reverse()])
     stream = torch.cuda.Stream()
