@@ -109,7 +109,10 @@ typedef struct hs_prog hs_prog;
 
 /* Creates the per-GPU context: binds `gpu`, allocates a symmetric arena of
  * `arena_bytes` of HBM (all shards, intermediates and staging live in it) and
- * a flag block for cross-rank barriers. */
+ * a flag block for cross-rank barriers.  Every rank must pass the same
+ * arena_bytes: an (rank, offset) pair names the same buffer everywhere only
+ * within the smallest arena (a rank sizing its arena from its own free memory
+ * must agree on the minimum with its peers first). */
 int hs_ctx_create(int rank, int world, int gpu, size_t arena_bytes, hs_ctx** out);
 void hs_ctx_destroy(hs_ctx* ctx);
 /* Base device pointer of this rank's arena. */
