@@ -423,10 +423,9 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     // fuses its local groups too (least HBM traffic) unless
     // HS_PROG_RELAY_KEEP_LOCAL asks to compute them before the barrier,
     // concurrently with the remote producers.
-    const bool keep = flags_ & HS_PROG_RELAY_KEEP_LOCAL;
-    const RelayMode mode = (flags_ & HS_PROG_PULL_MID) ? (keep ? RelayMode::PullBalance : RelayMode::Pull)
-                           : keep                      ? RelayMode::KeepLocal
-                                                       : RelayMode::FuseLocal;
+    const RelayMode mode = (flags_ & HS_PROG_PULL_MID)           ? RelayMode::Pull
+                           : (flags_ & HS_PROG_RELAY_KEEP_LOCAL) ? RelayMode::KeepLocal
+                                                                 : RelayMode::FuseLocal;
     tasks = finish(fuse_phases(std::move(tasks), mode));
     stats_.model_ms[0] = estimate_seconds(tasks, n_phases_) * 1e3;
     if (ce_mode_) tasks = ce_relay(std::move(tasks));
@@ -675,31 +674,6 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
     return Operand{relay_state, id};
   };
 
-  const bool pull = mode == RelayMode::Pull || mode == RelayMode::PullBalance;
-  // PullBalance: a rank whose pre-barrier work (the producers its peers pull
-  // from) is lighter than the busiest rank's also materialises the local
-  // groups of its own pulling tasks before the barrier, so that less HBM
-  // traffic contends with the NVLink pulls after it.
-  auto producer_bytes = [this](const BoxTask& P) {
-    return static_cast<int64_t>(P.box.cells()) * es_ * static_cast<int64_t>(P.terms.size() + P.dsts.size());
-  };
-  std::vector<char> counted(tasks.size(), 0);
-  std::vector<int64_t> pre_load(ctx_.world(), 0);
-  int64_t pre_max = 0;
-  if (mode == RelayMode::PullBalance) {
-    for (const BoxTask& T : tasks) {
-      if (T.phase != 1 || !T.groups.empty()) continue;
-      for (const Operand& o : T.terms)
-        if (o.state == mid_state_ && rank_of(o, T.tensor) != T.rank)
-          for (int p : producers[o.dev])
-            if (!counted[p] && intersect(tasks[p].box, T.box)) {
-              counted[p] = 1;
-              pre_load[tasks[p].rank] += producer_bytes(tasks[p]);
-            }
-    }
-    for (int64_t l : pre_load) pre_max = std::max(pre_max, l);
-  }
-
   std::vector<BoxTask> out;
   std::vector<char> keep_local(tasks.size(), 0);
   // producer -> consumer rank -> boxes that rank actually reads
@@ -729,7 +703,7 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
             for (const Operand& in : tasks[p].terms) fusable = fusable && rank_of(in, T.tensor) == q;
         }
       if (relay && rank_of(o, T.tensor) != q)
-        pol[j] = pull ? KEEP : RELAY;
+        pol[j] = mode == RelayMode::Pull ? KEEP : RELAY;
       else if (fusable && !prod[j].empty())
         pol[j] = FUSE;
     }
@@ -741,20 +715,6 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
     if (mode == RelayMode::KeepLocal && needs_relay)
       for (Policy& p : pol)
         if (p == FUSE) p = KEEP;
-    if (mode == RelayMode::PullBalance) {
-      bool pulls = false, light = true, any = false;
-      for (size_t j = 0; j < nt; ++j) {
-        pulls = pulls || (pol[j] == KEEP && T.terms[j].state == mid_state_ && rank_of(T.terms[j], T.tensor) != q);
-        if (pol[j] == FUSE)
-          for (int p : prod[j]) {
-            any = true;
-            light = light && pre_load[tasks[p].rank] < pre_max;
-          }
-      }
-      if (pulls && any && light)
-        for (Policy& p : pol)
-          if (p == FUSE) p = KEEP;
-    }
     auto build = [&](std::vector<BoxTask>& cells) {
       detail::Cuts cuts(T.box.bounds.size());
       for (size_t d = 0; d < cuts.size(); ++d) {

@@ -23,9 +23,7 @@ from paper_2504_20490_b200.executor import analyze
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 FLAG_SETS = [0, 14, 1, 32, 128, 256, 512, 1024, 1152, 2048, 2062, 4096, 8192, 12288, 16384, 16896,
-             32768, 32769, 32896, 16789504, 16790016]
-# last two: STATIC_LOCAL | PULL_MID | NO_STREAM, and the same with RELAY_KEEP_LOCAL
-# (pull-balance: lighter ranks materialise their local groups before the barrier)
+             32768, 32769, 32896, 16789504]  # last: STATIC_LOCAL | PULL_MID | NO_STREAM
 HEAVY = {"cfg3a", "cfg3c"}  # thousands of streamed pieces: default and unstreamed only
 NAMES = ["cfg1A", "cfg1B", "cfg1C", "cfg1D", "cfg2e", "cfg2a", "cfg2b", "cfg2d", "cfg3b", "cfg3a",
          "cfg3c", "cfg4"]
