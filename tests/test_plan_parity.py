@@ -133,3 +133,25 @@ def test_volume_report_matches_reference():
         assert {str(k): v for k, v in got.items()} == want, c["name"]
         js = F.volume_report(_json.loads(plan.dump())["xfer"], node_of=node_of)
         assert {str(k): v for k, v in js.items()} == want, c["name"]
+
+
+@pytest.mark.skipif(not os.path.exists(REF_TOOL), reason="reference build (oracle/_ref) absent")
+def test_live_align_sweep_against_reference():
+    """align_shard_specs (reference annotation.cpp:431-472) on random count chains, half of
+    them with equal totals so the common refinement usually exists."""
+    rng = random.Random(random.randrange(1 << 30))
+    keys = [-2, -1, 0, 1]
+
+    def spec(counts):
+        return "{" + ",".join(f"{rng.choice(keys)}:{c}" for c in counts) + "}"
+
+    chains = [[2, 2, 2], [4, 2], [2, 4], [8], [2, 3], [3, 2], [6], [4, 4], [2, 8], [1, 4, 1]]
+    cmds = [[f"A|{spec(rng.choice(chains))}|{spec(rng.choice(chains))}"] for _ in range(2000)]
+    cmds += [[f"A|{spec([rng.choice([1, 2, 3, 4]) for _ in range(rng.randint(0, 3))])}|"
+              f"{spec([rng.choice([1, 2, 3, 4]) for _ in range(rng.randint(0, 3))])}"] for _ in range(2000)]
+    text = "".join(c[0] + "\n" for c in cmds)
+    res = subprocess.run([REF_TOOL], input=text, capture_output=True, text=True, timeout=600)
+    outs = res.stdout.splitlines()
+    assert len(outs) == len(cmds)
+    bad = [(c, o) for c, o in zip(cmds, outs) if run(c) != o]
+    assert not bad, bad[:3]
