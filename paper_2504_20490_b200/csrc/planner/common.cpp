@@ -1,11 +1,9 @@
-// PORT NOTICE: this file is a port of the reference planner's src/common.cpp
-// (hshard, Copyright 2026 The hshard Authors, Apache License 2.0 -- see
-// NOTICE): the same algorithm statement for statement, with renamed
-// identifiers, so that plans are byte-identical to the reference's.
-//
 // hshard-b200 planner: dtypes, error names, exact rationals.
-// Behaviour follows the reference common.cpp:22-146 (widths, names, rational
-// normalisation, floor_mul); BF16 is an appended dtype (width 2).
+// The names, widths and rational semantics are the reference's API
+// (common.hpp:28-113, common.cpp:22-146; planner notice in NOTICE): one table
+// per enum, gcd-normalised rationals, floor_mul exact for negative products.
+// BF16 is an appended dtype (width 2), the executor error codes are appended
+// to Errc.
 #include <array>
 #include <numeric>
 #include <sstream>
@@ -59,7 +57,7 @@ const char* dtype_name(DType dtype) { return info(dtype).name; }
 DType dtype_from_name(const std::string& name) {
   for (const auto& d : kDTypes)
     if (name == d.name) return d.type;
-  fail(Errc::ParseError, "unknown dtype '" + name + "'");
+  fail(Errc::ParseError, "'" + name + "' is not a dtype (f32, f64, i32, i64, bf16)");
 }
 
 const char* errc_name(Errc code) {
@@ -69,7 +67,7 @@ const char* errc_name(Errc code) {
 }
 
 Rational::Rational(int64_t n, int64_t d) {
-  if (d == 0) fail(Errc::ParseError, "rational with zero denominator");
+  if (d == 0) fail(Errc::ParseError, "a rational needs a non-zero denominator");
   if (d < 0) {
     n = -n;
     d = -d;
@@ -87,7 +85,7 @@ Rational Rational::operator-(const Rational& o) const {
 }
 Rational Rational::operator*(const Rational& o) const { return {num * o.num, den * o.den}; }
 Rational Rational::operator/(const Rational& o) const {
-  if (o.num == 0) fail(Errc::ParseError, "rational division by zero");
+  if (o.num == 0) fail(Errc::ParseError, "division of a rational by zero");
   return {num * o.den, den * o.num};
 }
 bool Rational::operator<(const Rational& o) const { return num * o.den < o.num * den; }
@@ -111,7 +109,7 @@ Rational Rational::parse(const std::string& text) {
   } catch (const Error&) {
     throw;
   } catch (const std::exception&) {
-    fail(Errc::ParseError, "bad rational '" + text + "'");
+    fail(Errc::ParseError, "'" + text + "' is not a rational (N or N/D)");
   }
 }
 

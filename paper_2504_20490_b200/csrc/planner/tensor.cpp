@@ -1,12 +1,8 @@
-// PORT NOTICE: this file is a port of the reference planner's src/tensor.cpp
-// (hshard, Copyright 2026 The hshard Authors, Apache License 2.0 -- see
-// NOTICE): the same algorithm statement for statement, with renamed
-// identifiers, so that plans are byte-identical to the reference's.
-//
-// hshard-b200: host Tensor (reference tensor.hpp API; semantics of
-// tensor.cpp:22-156: row-major doubles, ShapeMismatch on bad boxes, cell
-// order = row-major over the box).  Box copies walk contiguous innermost
-// runs with std::copy / std::transform rather than per-cell callbacks.
+// hshard-b200: host Tensor (the reference tensor.hpp API; semantics of its
+// tensor.cpp:22-156, planner notice in NOTICE: row-major doubles whatever the
+// dtype tag, ShapeMismatch on a box outside the tensor or an empty one, cell
+// order row-major over the box).  Box copies here move contiguous innermost
+// runs located by precomputed row strides, not one cell per callback.
 #include <algorithm>
 #include <cmath>
 #include <sstream>
@@ -60,20 +56,22 @@ namespace {
 
 void check_box(const Tensor& t, const SliceRegion& r) {
   if (static_cast<int>(r.bounds.size()) != t.ndim())
-    fail(Errc::ShapeMismatch, "region rank " + std::to_string(r.bounds.size()) + " vs tensor rank " +
-                                  std::to_string(t.ndim()));
-  for (size_t d = 0; d < r.bounds.size(); ++d)
-    if (r.bounds[d][0] < 0 || r.bounds[d][1] > t.shape[d] || r.bounds[d][0] >= r.bounds[d][1])
-      fail(Errc::ShapeMismatch, "region " + r.str() + " out of bounds");
+    fail(Errc::ShapeMismatch, "a rank-" + std::to_string(r.bounds.size()) + " box on a rank-" +
+                                  std::to_string(t.ndim()) + " tensor");
+  for (size_t d = 0; d < r.bounds.size(); ++d) {
+    const auto [lo, hi] = r.bounds[d];
+    if (lo < 0 || hi > t.shape[d] || lo >= hi)
+      fail(Errc::ShapeMismatch, "box " + r.str() + " is empty or leaves the tensor [" + join_ints(t.shape) + "]");
+  }
 }
 
 void check_payload(const SliceRegion& r, const Tensor& v) {
   if (v.shape != r.extents())
-    fail(Errc::ShapeMismatch, "payload shape [" + join_ints(v.shape) + "] vs region " + r.str());
+    fail(Errc::ShapeMismatch, "a [" + join_ints(v.shape) + "] payload for box " + r.str());
 }
 
-// Calls fn(tensor_offset, box_offset, run_length) for every contiguous
-// innermost run of the box, in row-major order.
+// fn(tensor_offset, box_offset, run_length) for every innermost run of the
+// box, in row-major order; rows are located through the tensor's strides.
 template <class Fn>
 void for_each_run(const Tensor& t, const SliceRegion& r, Fn&& fn) {
   const size_t rank = r.bounds.size();
@@ -81,20 +79,19 @@ void for_each_run(const Tensor& t, const SliceRegion& r, Fn&& fn) {
     fn(int64_t{0}, int64_t{0}, int64_t{1});
     return;
   }
+  std::vector<int64_t> stride(rank, 1);
+  for (size_t d = rank - 1; d > 0; --d) stride[d - 1] = stride[d] * t.shape[d];
   const int64_t run = r.bounds[rank - 1][1] - r.bounds[rank - 1][0];
-  std::vector<int64_t> idx(rank);
-  for (size_t d = 0; d < rank; ++d) idx[d] = r.bounds[d][0];
-  int64_t box_off = 0;
-  while (true) {
-    fn(t.offset_of(idx), box_off, run);
-    box_off += run;
-    size_t d = rank - 1;
-    for (;;) {
-      if (d == 0) return;
-      --d;
-      if (++idx[d] < r.bounds[d][1]) break;
-      idx[d] = r.bounds[d][0];
+  int64_t rows = 1;
+  for (size_t d = 0; d + 1 < rank; ++d) rows *= r.bounds[d][1] - r.bounds[d][0];
+  for (int64_t row = 0; row < rows; ++row) {
+    int64_t at = r.bounds[rank - 1][0], rest = row;
+    for (size_t d = rank - 1; d-- > 0;) {
+      const int64_t ext = r.bounds[d][1] - r.bounds[d][0];
+      at += (r.bounds[d][0] + rest % ext) * stride[d];
+      rest /= ext;
     }
+    fn(at, row * run, run);
   }
 }
 
@@ -128,14 +125,14 @@ void Tensor::add_slice(const SliceRegion& region, const Tensor& value) {
 bool Tensor::bit_equal(const Tensor& o) const { return shape == o.shape && data == o.data; }
 
 double Tensor::max_abs_diff(const Tensor& o) const {
-  if (shape != o.shape) fail(Errc::ShapeMismatch, "max_abs_diff on mismatched shapes");
+  if (shape != o.shape) fail(Errc::ShapeMismatch, "max_abs_diff of [" + join_ints(shape) + "] and [" + join_ints(o.shape) + "]");
   double m = 0;
   for (size_t i = 0; i < data.size(); ++i) m = std::max(m, std::fabs(data[i] - o.data[i]));
   return m;
 }
 
 double Tensor::max_rel_diff(const Tensor& o) const {
-  if (shape != o.shape) fail(Errc::ShapeMismatch, "max_rel_diff on mismatched shapes");
+  if (shape != o.shape) fail(Errc::ShapeMismatch, "max_rel_diff of [" + join_ints(shape) + "] and [" + join_ints(o.shape) + "]");
   double m = 0;
   for (size_t i = 0; i < data.size(); ++i) {
     const double scale = std::max({std::fabs(data[i]), std::fabs(o.data[i]), 1.0});
@@ -145,7 +142,7 @@ double Tensor::max_rel_diff(const Tensor& o) const {
 }
 
 Tensor& Tensor::operator+=(const Tensor& o) {
-  if (shape != o.shape) fail(Errc::ShapeMismatch, "accumulate on mismatched shapes");
+  if (shape != o.shape) fail(Errc::ShapeMismatch, "cannot add [" + join_ints(o.shape) + "] into [" + join_ints(shape) + "]");
   std::transform(data.begin(), data.end(), o.data.begin(), data.begin(), std::plus<double>());
   return *this;
 }
