@@ -181,9 +181,14 @@ enum {
   HS_PROG_NO_PDL = 1 << 28,       /* launch phase kernels without programmatic dependent launch
                                      (default: each launch is scheduled while the previous one on
                                      the stream drains and waits for it on the device) */
-  HS_PROG_INTERLEAVE = 1 << 29    /* world > 1, unstreamed launches: items of tasks with NVLink
+  HS_PROG_INTERLEAVE = 1 << 29,   /* world > 1, unstreamed launches: items of tasks with NVLink
                                      operands and of local-only tasks are merged evenly in launch
                                      order (default: task order) -- the autotuner times it */
+  HS_PROG_SPLIT_RELAY = 1 << 30    /* world > 1, two-phase plans: a consumer's remote mid rows are
+                                     split in two bands -- the producers push the first band into
+                                     the consumer's relay buffer before the barrier, the consumer
+                                     pulls the second after it -- so the NVLink transfer is spread
+                                     over both phases; the autotuner times it */
 };
 /* Streamed programs: bits 16..23 of the flags = the share of CTAs that take
  * non-waiting work first, in 1/64 (0 = modelled from the phases' bytes). */

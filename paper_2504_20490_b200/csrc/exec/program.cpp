@@ -423,7 +423,8 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
     // fuses its local groups too (least HBM traffic) unless
     // HS_PROG_RELAY_KEEP_LOCAL asks to compute them before the barrier,
     // concurrently with the remote producers.
-    const RelayMode mode = (flags_ & HS_PROG_PULL_MID)           ? RelayMode::Pull
+    const RelayMode mode = (flags_ & HS_PROG_SPLIT_RELAY)        ? RelayMode::Split
+                           : (flags_ & HS_PROG_PULL_MID)           ? RelayMode::Pull
                            : (flags_ & HS_PROG_RELAY_KEEP_LOCAL) ? RelayMode::KeepLocal
                                                                  : RelayMode::FuseLocal;
     tasks = finish(fuse_phases(std::move(tasks), mode));
@@ -674,6 +675,12 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
     return Operand{relay_state, id};
   };
 
+  // Split: the boxes of each kept producer that some consumer actually reads
+  // locally (the other rows go out as relays only).
+  const bool split = mode == RelayMode::Split;
+  int64_t split_64ths = 32;  // share of the rows relayed (exploration knob)
+  if (const char* e = std::getenv("HS_SPLIT_RELAY_64THS")) split_64ths = std::clamp(std::atol(e), 1L, 63L);
+  std::vector<std::vector<SliceRegion>> keep_at(tasks.size());
   std::vector<BoxTask> out;
   std::vector<char> keep_local(tasks.size(), 0);
   // producer -> consumer rank -> boxes that rank actually reads
@@ -712,6 +719,17 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
     // instead of redoing them after the barrier.
     bool needs_relay = false;
     for (Policy p : pol) needs_relay = needs_relay || p == RELAY;
+    // Split: rows [lo, band) of the task read relays, rows [band, hi) pull.
+    const int64_t row_lo = T.box.bounds.empty() ? 0 : T.box.bounds[0][0];
+    const int64_t row_hi = T.box.bounds.empty() ? 0 : T.box.bounds[0][1];
+    const int64_t band = split && needs_relay && row_hi - row_lo >= 2
+                             ? std::clamp(row_lo + (row_hi - row_lo) * split_64ths / 64, row_lo + 1, row_hi - 1)
+                             : row_hi;
+    auto band_box = [&](bool first) {
+      SliceRegion b = T.box;
+      b.bounds[0] = first ? std::array<int64_t, 2>{row_lo, band} : std::array<int64_t, 2>{band, row_hi};
+      return b;
+    };
     if (mode == RelayMode::KeepLocal && needs_relay)
       for (Policy& p : pol)
         if (p == FUSE) p = KEEP;
@@ -725,6 +743,7 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
             for (int p : prod[j])
               for (int64_t v : tasks[p].box.bounds[d])
                 if (lo < v && v < hi) s.insert(v);
+        if (d == 0 && band < row_hi) s.insert(band);
         cuts[d].assign(s.begin(), s.end());
       }
       bool ok = true;
@@ -748,7 +767,8 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
             N.groups.push_back(static_cast<int>(src->terms.size()));
             nested = nested || src->terms.size() > 1;
           } else {
-            N.terms.push_back(pol[j] == RELAY ? relay_operand(T.terms[j].dev, q) : T.terms[j]);
+            const bool relayed = pol[j] == RELAY && cell.bounds[0][0] < band;
+            N.terms.push_back(relayed ? relay_operand(T.terms[j].dev, q) : T.terms[j]);
             N.groups.push_back(1);
           }
         }
@@ -772,6 +792,13 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
       for (int p : producers[T.terms[j].dev]) {
         if (pol[j] != RELAY) {
           keep_local[p] = 1;
+          if (auto need = intersect(tasks[p].box, T.box)) keep_at[p].push_back(*need);
+        } else if (band < row_hi) {  // split: first band relayed, second kept for the pull
+          if (auto need = intersect(tasks[p].box, band_box(true))) relay_to[p][q].push_back(*need);
+          if (auto need = intersect(tasks[p].box, band_box(false))) {
+            keep_local[p] = 1;
+            keep_at[p].push_back(*need);
+          }
         } else if (auto need = intersect(tasks[p].box, T.box)) {
           relay_to[p][q].push_back(*need);
         }
@@ -809,13 +836,22 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
         for (const SliceRegion& b : boxes)
           for (int64_t v : b.bounds[d])
             if (lo < v && v < hi) s.insert(v);
+      if (split)
+        for (const SliceRegion& b : keep_at[i])
+          for (int64_t v : b.bounds[d])
+            if (lo < v && v < hi) s.insert(v);
       cuts[d].assign(s.begin(), s.end());
     }
     detail::for_each_grid_cell(cuts, [&](const SliceRegion& cell) {
       BoxTask piece = P;
       piece.box = cell;
       piece.dsts.clear();
-      if (keep_local[i]) piece.dsts.push_back(P.dsts[0]);
+      bool local = keep_local[i];
+      if (split && local) {  // only the rows some consumer reads from the local mid
+        local = false;
+        for (const SliceRegion& b : keep_at[i]) local = local || b.covers(cell);
+      }
+      if (local) piece.dsts.push_back(P.dsts[0]);
       for (const auto& [q, boxes] : relay_to[i]) {
         bool read = false;
         for (const SliceRegion& b : boxes) read = read || b.covers(cell);

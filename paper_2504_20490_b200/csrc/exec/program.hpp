@@ -244,7 +244,7 @@ class Program {
   // None: world 1 fusion.  KeepLocal / FuseLocal: remote mid reads become
   // relays (producers store into the consumer's HBM).  Pull: remote mid
   // reads pull the producer's materialised mid box (local groups fused).
-  enum class RelayMode { None, KeepLocal, FuseLocal, Pull };
+  enum class RelayMode { None, KeepLocal, FuseLocal, Pull, Split };
   std::vector<BoxTask> fuse_phases(std::vector<BoxTask> tasks, RelayMode mode);
   double estimate_seconds(const std::vector<BoxTask>& tasks, int phases);
   void stage_for_nccl(std::vector<BoxTask>& tasks);

@@ -49,6 +49,7 @@ HS_PROG_SEPARATE_BARRIERS = 1 << 26  # world > 1: barriers as their own launches
 HS_PROG_SMALL_ITEMS = 1 << 27  # 16 KB TMA work items (plan-dependent; autotuned at N=1)
 HS_PROG_NO_PDL = 1 << 28  # no programmatic dependent launch between phase kernels (A/B)
 HS_PROG_INTERLEAVE = 1 << 29  # world > 1: NVLink and local-only items merged evenly in launch order
+HS_PROG_SPLIT_RELAY = 1 << 30  # world > 1: remote mid rows half pushed before the barrier, half pulled after
 HS_PROG_BASELINE = HS_PROG_NO_FUSE | HS_PROG_NO_TMA | HS_PROG_NO_MERGE
 
 NP_STORAGE = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64,

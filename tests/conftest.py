@@ -24,9 +24,10 @@ def cuda_available() -> bool:
         return False
 
 
-@pytest.fixture(scope="session")
+@pytest.fixture(scope="module")
 def gpu_ctx():
-    """One executor context on cuda:0 for the whole GPU test session."""
+    """One executor context on cuda:0 per test module (closed before the
+    multi-GPU tests, whose rank 0 needs that memory on the same GPU)."""
     if not cuda_available():
         pytest.skip("no GPU")
     import torch
