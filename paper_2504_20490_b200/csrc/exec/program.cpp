@@ -767,7 +767,7 @@ std::vector<BoxTask> Program::fuse_phases(std::vector<BoxTask> tasks, RelayMode 
             N.groups.push_back(static_cast<int>(src->terms.size()));
             nested = nested || src->terms.size() > 1;
           } else {
-            const bool relayed = pol[j] == RELAY && cell.bounds[0][0] < band;
+            const bool relayed = pol[j] == RELAY && (cell.bounds.empty() || cell.bounds[0][0] < band);
             N.terms.push_back(relayed ? relay_operand(T.terms[j].dev, q) : T.terms[j]);
             N.groups.push_back(1);
           }

@@ -54,7 +54,7 @@ def _release_parent_gpu_memory():
                                    # after it: alone, with static dealing, streamed
                                    "1073745920,1090523136,1073741824",
                                    # 60 random plans of every kind and dtype through several variants
-                                   "random:0,14,1,12288,536870912",
+                                   "random:0,14,1,12288,536870912,1073745920",
                                    # BASELINE reduction configs at FULL size, real-valued payloads,
                                    # vs the native CPU executor: default, plain, pull-mid, fused
                                    "full:0,14,12288,1"])
