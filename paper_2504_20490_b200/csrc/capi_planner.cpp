@@ -1,5 +1,6 @@
 // hshard-b200 C ABI: planner entry points (include/hshard_c.h).
 #include <chrono>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstdlib>
@@ -70,11 +71,18 @@ int hs_plan_switch(int n, const int* tensor_ids, const char* const* src, const c
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<SwitchEntry> diff;
     const int64_t* cursor = shapes_flat;
+    // a model repeats a handful of annotation texts: parse each once
+    std::unordered_map<std::string, HetAnnotation> parsed;
+    auto anno = [&](const char* text) -> const HetAnnotation& {
+      auto it = parsed.find(text);
+      if (it == parsed.end()) it = parsed.emplace(text, parse_annotation(text)).first;
+      return it->second;
+    };
     for (int i = 0; i < n; ++i) {
       SwitchEntry e;
       e.tensor_id = tensor_ids[i];
-      e.src = parse_annotation(src[i]);
-      e.dst = parse_annotation(dst[i]);
+      e.src = anno(src[i]);
+      e.dst = anno(dst[i]);
       e.shape = to_shape(cursor, ndims[i]);
       cursor += ndims[i];
       diff.push_back(std::move(e));

@@ -157,34 +157,52 @@ std::vector<FusionGroup> fusion_groups(const std::vector<Transfer>& xfer) {
   return groups;
 }
 
-BsrPlan plan_rows(const std::vector<const BsrRow*>& rows, const Bandwidth* bw) {
+// A row as the planner sees it: the tensor it belongs to may differ from the
+// table row's own tensor_id when one table serves several identical tensors.
+struct RowRef {
+  int tensor;
+  const BsrRow* row;
+};
+
+BsrPlan plan_rows(const std::vector<RowRef>& rows, const Bandwidth* bw) {
   BsrPlan plan;
   SenderChooser chooser(bw);
-  for (const BsrRow* row : rows) {
+  std::vector<DeviceId> owners, receivers;
+  for (const auto& [tensor, row] : rows) {
     if (row->requesters.empty()) continue;
     if (row->owners.empty())
-      fail(Errc::NoOwner, "nobody holds " + row->region.str() + " of tensor " + std::to_string(row->tensor_id));
-    std::vector<DeviceId> owners = row->owners, receivers = row->requesters;
+      fail(Errc::NoOwner, "nobody holds " + row->region.str() + " of tensor " + std::to_string(tensor));
+    owners.assign(row->owners.begin(), row->owners.end());
+    receivers.assign(row->requesters.begin(), row->requesters.end());
     std::sort(owners.begin(), owners.end());
     std::sort(receivers.begin(), receivers.end());
     for (DeviceId r : receivers) {
       if (std::binary_search(owners.begin(), owners.end(), r)) {
-        plan.local_copies.push_back({r, row->tensor_id, row->region});
+        plan.local_copies.push_back({r, tensor, row->region});
         continue;
       }
-      const DeviceId s = chooser.choose(owners, r);
-      plan.transfers.push_back({row->tensor_id, row->region, s, r, row->bytes});
-      chooser.charge(s, row->bytes);
+      const DeviceId snd = chooser.choose(owners, r);
+      plan.transfers.push_back({tensor, row->region, snd, r, row->bytes});
+      chooser.charge(snd, row->bytes);
     }
   }
   plan.fusion_groups = fusion_groups(plan.transfers);
   return plan;
 }
 
-std::vector<const BsrRow*> rows_of(const BsrTable& t) {
-  std::vector<const BsrRow*> v(t.rows.size());
-  std::transform(t.rows.begin(), t.rows.end(), v.begin(), [](const BsrRow& r) { return &r; });
+std::vector<RowRef> rows_of(const BsrTable& t) {
+  std::vector<RowRef> v;
+  v.reserve(t.rows.size());
+  for (const BsrRow& r : t.rows) v.push_back({r.tensor_id, &r});
   return v;
+}
+
+// fuse over (tensor, table) pairs: rows ordered by (tensor, region bounds).
+BsrPlan fuse_rows(std::vector<RowRef> rows, const Bandwidth& bw) {
+  std::stable_sort(rows.begin(), rows.end(), [](const RowRef& a, const RowRef& b) {
+    return a.tensor != b.tensor ? a.tensor < b.tensor : a.row->region.bounds < b.row->region.bounds;
+  });
+  return plan_rows(rows, &bw);
 }
 
 }  // namespace
@@ -196,19 +214,32 @@ BsrPlan make_plan_naive(const BsrTable& table) { return plan_rows(rows_of(table)
 BsrPlan fuse(const std::vector<BsrTable>& tables, const Bandwidth& bandwidth) {
   // every tensor id belongs to one table
   std::map<int, size_t> owner_table;
-  std::vector<const BsrRow*> rows;
+  std::vector<RowRef> rows;
   for (size_t k = 0; k < tables.size(); ++k)
     for (const BsrRow& r : tables[k].rows) {
       const auto [it, fresh] = owner_table.emplace(r.tensor_id, k);
       if (!fresh && it->second != k)
         fail(Errc::ParseError, "tensor " + std::to_string(r.tensor_id) + " appears in two fused tables");
-      rows.push_back(&r);
+      rows.push_back({r.tensor_id, &r});
     }
-  std::stable_sort(rows.begin(), rows.end(), [](const BsrRow* a, const BsrRow* b) {
-    return std::tie(a->tensor_id, a->region.bounds) < std::tie(b->tensor_id, b->region.bounds);
-  });
-  return plan_rows(rows, &bandwidth);
+  return fuse_rows(std::move(rows), bandwidth);
 }
+
+namespace detail {
+
+BsrPlan fuse_relabelled(const std::vector<std::pair<int, const BsrTable*>>& tables, const Bandwidth& bandwidth) {
+  std::set<int> ids;
+  std::vector<RowRef> rows;
+  for (const auto& [tensor, table] : tables) {
+    if (table->rows.empty()) continue;
+    if (!ids.insert(tensor).second)
+      fail(Errc::ParseError, "tensor " + std::to_string(tensor) + " appears in two fused tables");
+    for (const BsrRow& r : table->rows) rows.push_back({tensor, &r});
+  }
+  return fuse_rows(std::move(rows), bandwidth);
+}
+
+}  // namespace detail
 
 std::map<DeviceId, VolumeEntry> volume_report(const BsrPlan& plan, const std::map<DeviceId, int>& node_of) {
   std::map<DeviceId, VolumeEntry> report;

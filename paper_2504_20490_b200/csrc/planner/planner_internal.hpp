@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "hshard/annotation.hpp"
+#include "hshard/bsr.hpp"
 
 namespace hshard::detail {
 
@@ -82,5 +83,10 @@ class CoverGrid {
   std::vector<std::vector<CoverSet>> along_;  // [dim][interval]: boxes spanning it
   size_t nboxes_ = 0;
 };
+
+// fuse() over tables shared by several tensors: entry (t, table) contributes
+// table's rows labelled as tensor t (no copies); same plan as fuse() over
+// relabelled copies of the tables.
+BsrPlan fuse_relabelled(const std::vector<std::pair<int, const BsrTable*>>& tables, const Bandwidth& bandwidth);
 
 }  // namespace hshard::detail

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "hshard/graph.hpp"
+#include "planner_internal.hpp"
 
 namespace hshard {
 
@@ -44,9 +45,10 @@ SwitchPlan plan_switch(const std::vector<SwitchEntry>& diff, DType dtype,
   // depends on the tensor only through BsrRow::tensor_id, so each distinct
   // triple is built once and its rows relabelled (same table, same order).
   const auto t0 = std::chrono::steady_clock::now();
-  std::vector<BsrTable> tables;
-  tables.reserve(diff.size());
-  std::unordered_map<std::string, size_t> seen;  // triple -> index of its first table
+  std::vector<BsrTable> distinct;
+  std::vector<std::pair<int, size_t>> uses;  // (tensor id, index into distinct)
+  uses.reserve(diff.size());
+  std::unordered_map<std::string, size_t> seen;  // triple -> its table
   for (const SwitchEntry& e : diff) {
     std::string key = e.src.str();
     key += '>';
@@ -55,20 +57,21 @@ SwitchPlan plan_switch(const std::vector<SwitchEntry>& diff, DType dtype,
     key += join_ints(e.shape);
     auto it = seen.find(key);
     if (it == seen.end()) {
-      seen.emplace(std::move(key), tables.size());
-      tables.push_back(build_table(e.src, e.dst, e.shape, e.tensor_id, dtype_width(dtype)));
-    } else {
-      BsrTable t = tables[it->second];
-      for (BsrRow& r : t.rows) r.tensor_id = e.tensor_id;
-      tables.push_back(std::move(t));
+      it = seen.emplace(std::move(key), distinct.size()).first;
+      distinct.push_back(build_table(e.src, e.dst, e.shape, e.tensor_id, dtype_width(dtype)));
     }
+    uses.emplace_back(e.tensor_id, it->second);
   }
+  std::vector<std::pair<int, const BsrTable*>> tables;
+  tables.reserve(uses.size());
+  for (const auto& [tid, k] : uses) tables.emplace_back(tid, &distinct[k]);
   const auto t1 = std::chrono::steady_clock::now();
-  sp.plan = fuse(tables, bandwidth);
+  sp.plan = detail::fuse_relabelled(tables, bandwidth);
   if (std::getenv("HS_COMPILE_TRACE"))
-    std::fprintf(stderr, "[plan] build_table %.2f ms, fuse %.2f ms (%zu tables)\n",
+    std::fprintf(stderr, "[plan] build_table %.2f ms, fuse %.2f ms (%zu tables, %zu distinct)\n",
                  std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(), tables.size());
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(), tables.size(),
+                 distinct.size());
   return sp;
 }
 
