@@ -92,10 +92,19 @@ int64_t cells_of(const SliceRegion& r) { return r.cells(); }
 }  // namespace
 
 ShardLoc& Program::loc(int state, int tensor, DeviceId d) {
+  const bool dense = tensor >= 0 && tensor < n_tensors_ && d >= 0 && d < n_virt_;
+  const size_t slot = dense ? static_cast<size_t>(tensor) * n_virt_ + d : 0;
+  if (dense && static_cast<size_t>(state) < dense_.size() && !dense_[state].empty())
+    if (ShardLoc* p = dense_[state][slot]) return *p;
   auto it = states_[state].find({tensor, d});
   if (it == states_[state].end())
     fail(Errc::MissingShard, "no shard for tensor slot " + std::to_string(tensor) + " on device " +
                                  std::to_string(d));
+  if (dense) {
+    if (dense_.size() <= static_cast<size_t>(state)) dense_.resize(state + 1);
+    if (dense_[state].empty()) dense_[state].assign(static_cast<size_t>(n_tensors_) * n_virt_, nullptr);
+    dense_[state][slot] = &it->second;
+  }
   return it->second;
 }
 

@@ -278,6 +278,9 @@ class Program {
   std::vector<Shape> shapes_;
   // layout states: 0 = src, 1 = mid (CommPlan with mid) / dst, 2 = dst
   std::vector<std::map<std::pair<int, DeviceId>, ShardLoc>> states_;
+  // loc() cache: per state, [tensor * n_virt + dev] -> map node (map nodes
+  // never move and are never erased), filled on first lookup
+  std::vector<std::vector<ShardLoc*>> dense_;
   int n_phases_ = 0;
   std::vector<DevicePhase> dphases_;
   void* dev_block_ = nullptr;
