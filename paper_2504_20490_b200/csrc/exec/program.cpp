@@ -174,7 +174,8 @@ Program::Program(Context& ctx, const CommPlan* comm, const SwitchPlan* sw,
       }
       L.subgroup = a.subgroup_of(d);
       L.eff_hdim = a.effective_hdim();
-      states_[state][{t, d}] = L;
+      auto& m = states_[state];  // keys arrive in ascending (tensor, device) order
+      m.insert_or_assign(m.end(), std::pair<int, DeviceId>{t, d}, L);
     }
   };
   for (int t = 0; t < n_tensors_; ++t) {
@@ -386,7 +387,7 @@ void Program::lower(const CommPlan* comm, const SwitchPlan* sw) {
   if (ce_mode_) {
     // producers run where their mid box lives; nothing else stores remotely
     flags_ |= HS_PROG_NO_SHARE | HS_PROG_PULL_COPIES;
-    flags_ &= ~(HS_PROG_PUSH_ALL | HS_PROG_FUSE_PHASES | HS_PROG_PULL_MID | HS_PROG_NO_RELAY);
+    flags_ &= ~(HS_PROG_PUSH_ALL | HS_PROG_FUSE_PHASES | HS_PROG_PULL_MID | HS_PROG_NO_RELAY | HS_PROG_SPLIT_RELAY);
     if (const char* e = std::getenv("HS_CE_CHUNKS")) ce_chunks_ = std::max(1, std::atoi(e));
   }
   if (ctx_.world() > 1 && !(flags_ & HS_PROG_NO_REPLICA)) choose_replicas(tasks);
