@@ -466,7 +466,12 @@ class StrategyCycle:
     step k's destinations are step k+1's sources; when the last step returns to the
     first strategy the cycle reuses the first state's placement."""
 
-    def __init__(self, ctx: Context, steps, dtype: str, n_virtual: int, flags: int = 0):
+    def __init__(self, ctx: Context, steps, dtype: str, n_virtual: int, flags: Optional[int] = None):
+        # Untuned default across GPUs: every copy runs on the rank that holds its input
+        # (switch plans are copy-only).  In the N=2 / N=4 sweeps it is never more than
+        # 0.5% slower than flags 0 and up to 1.7x faster (cfg5 S1->S2, S2->S3).
+        if flags is None:
+            flags = HS_PROG_PUSH_ALL if ctx.world > 1 else 0
         self.ctx, self.steps, self.dtype, self.n_virtual, self.flags = ctx, steps, dtype, n_virtual, flags
         ents = [[(i, tid, s, shp) for i, (tid, s, d, shp) in enumerate(st)] for st in steps]
         ents.append([(i, tid, d, shp) for i, (tid, s, d, shp) in enumerate(steps[-1])])

@@ -203,6 +203,42 @@ def main():
         results.append({"case": "pointers", "flags": 0, "bad": bad, "nvlink_in": 0, "nvlink_out": 0})
         return not bad
 
+    def cycle_case():
+        """executor.StrategyCycle across GPUs: the cfg5 4-strategy cycle (shapes / 32) twice,
+        with the default variant (PUSH_ALL at N > 1) and with flags 0, step k+1 planned and
+        compiled while step k runs (the pipelined pattern); every state verified on-device
+        on every rank, the second round served from the plan/program cache."""
+        from paper_2504_20490_b200.executor import StrategyCycle
+        steps = [[(tid, s, d, tuple(max(8, v // 32) for v in shp)) for tid, s, d, shp in W.config5(x).transitions]
+                 for x in W.CONFIG5_CYCLE]
+        bad = []
+        for flags in (None, 0):
+            mark = ctx.alloc(0)
+            cyc = StrategyCycle(ctx, steps, "bf16", 8, flags)
+            try:
+                cyc.states[0].fill(7)
+                ctx.sync()
+                dist.barrier()
+                for rnd in range(2):
+                    prog, info = cyc.prepare(0)
+                    if info["program_cached"] != (rnd == 1):
+                        bad.append(("cache", flags, rnd))
+                    for k in range(len(steps)):
+                        prog.run()  # enqueues only: the next step compiles meanwhile
+                        nxt = cyc.prepare(k + 1)[0] if k + 1 < len(steps) else None
+                        ctx.sync()
+                        dist.barrier()
+                        b = cyc.states[k + 1].verify(7)
+                        if b:
+                            bad.append((cyc.flags, rnd, k, b))
+                        prog = nxt
+            finally:
+                dist.barrier()
+                cyc.close()
+                ctx.reset(mark)
+        results.append({"case": "strategy-cycle", "flags": -1, "bad": bad, "nvlink_in": 0, "nvlink_out": 0})
+        return not bad
+
     def random_cases():
         """Random plans of every step kind and dtype (tests/golden/gen_cases.rand_pair,
         the same seeded list on every rank), 10 virtual devices block-mapped onto the
@@ -245,6 +281,8 @@ def main():
         if not host_path_case():
             ok = False
         if not pointer_case():
+            ok = False
+        if not cycle_case():
             ok = False
         for wname, shape in [("cfg1A", (256, 64)), ("cfg1B", (256, 64)), ("cfg1D", (256, 64)),
                              ("cfg2e", (64, 256)), ("cfg2b", (64, 256)), ("cfg3b", (64, 512)),
