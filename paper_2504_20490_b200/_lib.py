@@ -12,6 +12,8 @@ from ctypes import POINTER, c_char_p, c_int, c_int64, c_size_t, c_uint32, c_ulon
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libhshard_b200.so")
+if os.environ.get("HS_LIB_VARIANT"):  # exploration builds only (tools/stage_sweep.sh)
+    LIB_PATH = os.path.join(_HERE, "lib", "variants", os.environ["HS_LIB_VARIANT"], "libhshard_b200.so")
 
 ERRC_NAMES = [
     "OverlappingSubgroups", "CardinalityMismatch", "BadSplitDim", "IndivisibleSplit",

@@ -141,8 +141,14 @@ struct PhaseTables {
 // Shared-memory staging of the TMA kernel: kStages ring buffers of
 // kStageBytes; the host sizes 16-byte-vector items so that
 // nterms * nrow * nvcol * 16 <= kStageBytes.
-inline constexpr int kTmaStages = 4;
-inline constexpr int kStageBytes = 48 * 1024;
+#ifndef HS_TMA_STAGES  // exploration builds override these (tools/stage_sweep.sh)
+#define HS_TMA_STAGES 4
+#endif
+#ifndef HS_STAGE_KB
+#define HS_STAGE_KB 48
+#endif
+inline constexpr int kTmaStages = HS_TMA_STAGES;
+inline constexpr int kStageBytes = HS_STAGE_KB * 1024;
 
 // dtype codes follow hshard::DType (F32, F64, I32, I64, BF16).
 // `tma`: items were sized for the TMA pipeline (16-byte vectors only).
