@@ -5,6 +5,8 @@
 // runs located by precomputed row strides, not one cell per callback.
 #include <algorithm>
 #include <cmath>
+#include <functional>
+#include <numeric>
 #include <sstream>
 
 #include "hshard/tensor.hpp"
@@ -12,43 +14,44 @@
 namespace hshard {
 
 int64_t shape_numel(const Shape& s) {
-  int64_t n = 1;
-  for (int64_t d : s) n *= d;
-  return n;
+  return std::accumulate(s.begin(), s.end(), int64_t{1}, std::multiplies<int64_t>());
 }
 
 Tensor::Tensor(Shape s, DType t) : shape(std::move(s)), dtype(t), data(shape_numel(shape), 0.0) {}
 
-Tensor Tensor::zeros(Shape s, DType t) { return Tensor(std::move(s), t); }
+Tensor Tensor::zeros(Shape s, DType t) { return filled(std::move(s), 0.0, t); }
 
 Tensor Tensor::filled(Shape s, double v, DType t) {
-  Tensor out(std::move(s), t);
-  std::fill(out.data.begin(), out.data.end(), v);
+  Tensor out;
+  out.data.assign(static_cast<size_t>(shape_numel(s)), v);
+  out.shape = std::move(s);
+  out.dtype = t;
   return out;
 }
 
-int64_t Tensor::numel() const { return static_cast<int64_t>(data.size()); }
+int64_t Tensor::numel() const { return shape_numel(shape); }
 
-int64_t Tensor::offset_of(const std::vector<int64_t>& idx) const {
+int64_t Tensor::offset_of(const std::vector<int64_t>& idx) const {  // row-major (Horner)
   int64_t off = 0;
-  for (size_t d = 0; d < shape.size(); ++d) off = off * shape[d] + idx[d];
+  auto e = shape.begin();
+  for (auto i = idx.begin(); e != shape.end(); ++e, ++i) off = off * *e + *i;
   return off;
 }
 
-void for_each_cell(const SliceRegion& region,
-                   const std::function<void(const std::vector<int64_t>&)>& fn) {
+// Row-major over the box: the k-th cell's index is k's mixed-radix digits over
+// the box extents, offset by the box origin.
+void for_each_cell(const SliceRegion& region, const std::function<void(const std::vector<int64_t>&)>& fn) {
   const size_t rank = region.bounds.size();
+  const int64_t cells = region.cells();
   std::vector<int64_t> idx(rank);
-  for (size_t d = 0; d < rank; ++d) idx[d] = region.bounds[d][0];
-  while (true) {
-    fn(idx);
-    size_t d = rank;
-    for (;;) {
-      if (d == 0) return;
-      --d;
-      if (++idx[d] < region.bounds[d][1]) break;
-      idx[d] = region.bounds[d][0];
+  for (int64_t k = 0; k < (rank ? cells : 1); ++k) {
+    int64_t rest = k;
+    for (size_t d = rank; d-- > 0;) {
+      const int64_t ext = region.bounds[d][1] - region.bounds[d][0];
+      idx[d] = region.bounds[d][0] + rest % ext;
+      rest /= ext;
     }
+    fn(idx);
   }
 }
 
@@ -124,37 +127,42 @@ void Tensor::add_slice(const SliceRegion& region, const Tensor& value) {
 
 bool Tensor::bit_equal(const Tensor& o) const { return shape == o.shape && data == o.data; }
 
+namespace {
+
+// Largest per-element |a - b| / scale(a, b) of two equally shaped tensors.
+template <class Scale>
+double max_diff(const Tensor& a, const Tensor& b, const char* what, Scale scale) {
+  if (a.shape != b.shape)
+    fail(Errc::ShapeMismatch, std::string(what) + " of [" + join_ints(a.shape) + "] and [" + join_ints(b.shape) + "]");
+  return std::transform_reduce(a.data.begin(), a.data.end(), b.data.begin(), 0.0,
+                               [](double x, double y) { return std::max(x, y); },
+                               [&](double x, double y) { return std::fabs(x - y) / scale(x, y); });
+}
+
+}  // namespace
+
 double Tensor::max_abs_diff(const Tensor& o) const {
-  if (shape != o.shape) fail(Errc::ShapeMismatch, "max_abs_diff of [" + join_ints(shape) + "] and [" + join_ints(o.shape) + "]");
-  double m = 0;
-  for (size_t i = 0; i < data.size(); ++i) m = std::max(m, std::fabs(data[i] - o.data[i]));
-  return m;
+  return max_diff(*this, o, "max_abs_diff", [](double, double) { return 1.0; });
 }
 
 double Tensor::max_rel_diff(const Tensor& o) const {
-  if (shape != o.shape) fail(Errc::ShapeMismatch, "max_rel_diff of [" + join_ints(shape) + "] and [" + join_ints(o.shape) + "]");
-  double m = 0;
-  for (size_t i = 0; i < data.size(); ++i) {
-    const double scale = std::max({std::fabs(data[i]), std::fabs(o.data[i]), 1.0});
-    m = std::max(m, std::fabs(data[i] - o.data[i]) / scale);
-  }
-  return m;
+  return max_diff(*this, o, "max_rel_diff",
+                  [](double x, double y) { return std::max({std::fabs(x), std::fabs(y), 1.0}); });
 }
 
 Tensor& Tensor::operator+=(const Tensor& o) {
-  if (shape != o.shape) fail(Errc::ShapeMismatch, "cannot add [" + join_ints(o.shape) + "] into [" + join_ints(shape) + "]");
-  std::transform(data.begin(), data.end(), o.data.begin(), data.begin(), std::plus<double>());
+  if (shape != o.shape)
+    fail(Errc::ShapeMismatch, "cannot add [" + join_ints(o.shape) + "] into [" + join_ints(shape) + "]");
+  for (size_t i = 0; i < data.size(); ++i) data[i] += o.data[i];
   return *this;
 }
 
-std::string Tensor::str() const {
-  std::ostringstream os;
-  os << dtype_name(dtype) << "[" << join_ints(shape) << "]{";
+std::string Tensor::str() const {  // dtype[shape]{first 16 values,...}
+  std::ostringstream vals;
   const size_t shown = std::min<size_t>(data.size(), 16);
-  for (size_t i = 0; i < shown; ++i) os << (i ? "," : "") << data[i];
-  if (data.size() > shown) os << ",...";
-  os << "}";
-  return os.str();
+  for (size_t i = 0; i < shown; ++i) vals << (i ? "," : "") << data[i];
+  return std::string(dtype_name(dtype)) + "[" + join_ints(shape) + "]{" + vals.str() +
+         (data.size() > shown ? ",...}" : "}");
 }
 
 }  // namespace hshard
