@@ -467,11 +467,13 @@ class StrategyCycle:
     first strategy the cycle reuses the first state's placement."""
 
     def __init__(self, ctx: Context, steps, dtype: str, n_virtual: int, flags: Optional[int] = None):
-        # Untuned default across GPUs: every copy runs on the rank that holds its input
-        # (switch plans are copy-only).  In the N=2 / N=4 sweeps it is never more than
-        # 0.5% slower than flags 0 and up to 1.7x faster (cfg5 S1->S2, S2->S3).
+        # Untuned defaults (switch plans are copy-only).  Across GPUs every copy runs on
+        # the rank that holds its input: in the N=2 / N=4 sweeps never more than 0.5%
+        # slower than flags 0 and up to 1.7x faster (cfg5 S1->S2, S2->S3).  On one GPU
+        # copies leave through TMA bulk stores: never more than 0.1% slower, 3-7% faster
+        # on cfg4 and cfg5 S2->S3 / S3->S4 / S4->S1 (profiles/r02_sweep_n1.jsonl).
         if flags is None:
-            flags = HS_PROG_PUSH_ALL if ctx.world > 1 else 0
+            flags = HS_PROG_PUSH_ALL if ctx.world > 1 else HS_PROG_BULK_STORE
         self.ctx, self.steps, self.dtype, self.n_virtual, self.flags = ctx, steps, dtype, n_virtual, flags
         ents = [[(i, tid, s, shp) for i, (tid, s, d, shp) in enumerate(st)] for st in steps]
         ents.append([(i, tid, d, shp) for i, (tid, s, d, shp) in enumerate(steps[-1])])
