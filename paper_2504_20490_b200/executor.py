@@ -467,13 +467,16 @@ class StrategyCycle:
     first strategy the cycle reuses the first state's placement."""
 
     def __init__(self, ctx: Context, steps, dtype: str, n_virtual: int, flags: Optional[int] = None):
-        # Untuned defaults (switch plans are copy-only).  Across GPUs every copy runs on
-        # the rank that holds its input: in the N=2 / N=4 sweeps never more than 0.5%
-        # slower than flags 0 and up to 1.7x faster (cfg5 S1->S2, S2->S3).  On one GPU
-        # copies leave through TMA bulk stores: never more than 0.1% slower, 3-7% faster
-        # on cfg4 and cfg5 S2->S3 / S3->S4 / S4->S1 (profiles/r02_sweep_n1.jsonl).
+        # Untuned defaults (switch plans are copy-only).  Across GPUs: every copy runs on
+        # the rank holding its input, no cross-rank chunking, NVLink and local items
+        # interleaved, bulk stores -- within 2.3% of the best measured variant on every
+        # cfg4 / cfg5 step at N=2 and N=4 and up to 1.7x faster than flags 0
+        # (profiles/r02_cycle_flags_n{2,4}.jsonl).  On one GPU copies leave through TMA
+        # bulk stores: never more than 0.1% slower than flags 0, 3-7% faster on cfg4 and
+        # cfg5 S2->S3 / S3->S4 / S4->S1 (profiles/r02_sweep_n1.jsonl).
         if flags is None:
-            flags = HS_PROG_PUSH_ALL if ctx.world > 1 else HS_PROG_BULK_STORE
+            flags = (HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_INTERLEAVE | HS_PROG_BULK_STORE
+                     if ctx.world > 1 else HS_PROG_BULK_STORE)
         self.ctx, self.steps, self.dtype, self.n_virtual, self.flags = ctx, steps, dtype, n_virtual, flags
         ents = [[(i, tid, s, shp) for i, (tid, s, d, shp) in enumerate(st)] for st in steps]
         ents.append([(i, tid, d, shp) for i, (tid, s, d, shp) in enumerate(steps[-1])])
