@@ -638,9 +638,12 @@ AUTOTUNE_CANDIDATES = [0, HS_PROG_PULL_COPIES, HS_PROG_NO_SHARE, HS_PROG_NO_SHAR
                        HS_PROG_INTERLEAVE | HS_PROG_RELAY_KEEP_LOCAL | HS_PROG_NO_STREAM,
                        HS_PROG_INTERLEAVE | HS_PROG_NO_STREAM,
                        HS_PROG_INTERLEAVE | HS_PROG_PULL_MID | HS_PROG_NO_STREAM,
-                       # remote mid rows half relayed before the barrier, half pulled after it
+                       # remote mid rows half relayed before the barrier, half pulled after it;
+                       # with NVLink and local items interleaved in each launch
                        HS_PROG_SPLIT_RELAY | HS_PROG_NO_STREAM,
-                       HS_PROG_SPLIT_RELAY | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL]
+                       HS_PROG_SPLIT_RELAY | HS_PROG_NO_STREAM | HS_PROG_STATIC_LOCAL,
+                       HS_PROG_SPLIT_RELAY | HS_PROG_NO_STREAM | HS_PROG_INTERLEAVE,
+                       HS_PROG_SPLIT_RELAY | HS_PROG_NO_STREAM | HS_PROG_INTERLEAVE | HS_PROG_STATIC_LOCAL]
 AUTOTUNE_CANDIDATES_1GPU = [0, HS_PROG_BULK_STORE, HS_PROG_SMALL_ITEMS, HS_PROG_SMALL_ITEMS | HS_PROG_BULK_STORE]
 TUNE_MARGIN = 0.01  # a later candidate must beat the best so far by 1% (timing noise)
 # HS_PROG_CE_RELAY is correct (tests/test_multi_gpu.py) but measured slower on every

@@ -51,10 +51,10 @@ def _release_parent_gpu_memory():
                                    # NVLink / local items interleaved: alone, keep-local relays, pull-mid
                                    "536870912,536875520,536883200",
                                    # remote mid rows half relayed before the barrier, half pulled
-                                   # after it: alone, with static dealing, streamed
-                                   "1073745920,1090523136,1073741824",
+                                   # after it: alone, with static dealing, streamed, interleaved
+                                   "1073745920,1090523136,1073741824,1610616832,1627394048",
                                    # 60 random plans of every kind and dtype through several variants
-                                   "random:0,14,1,12288,536870912,1073745920",
+                                   "random:0,14,1,12288,536870912,1073745920,1610616832",
                                    # BASELINE reduction configs at FULL size, real-valued payloads,
                                    # vs the native CPU executor: default, plain, pull-mid, fused
                                    "full:0,14,12288,1"])

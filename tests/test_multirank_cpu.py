@@ -23,8 +23,8 @@ from paper_2504_20490_b200.executor import analyze
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 FLAG_SETS = [0, 14, 1, 32, 128, 256, 512, 1024, 1152, 2048, 2062, 4096, 8192, 12288, 16384, 16896,
-             32768, 32769, 32896, 16789504, 1073745920]
-# last two: STATIC_LOCAL | PULL_MID | NO_STREAM; SPLIT_RELAY | NO_STREAM
+             32768, 32769, 32896, 16789504, 1073745920, 1610616832]
+# last three: STATIC_LOCAL | PULL_MID | NO_STREAM; SPLIT_RELAY | NO_STREAM; the same + INTERLEAVE
 HEAVY = {"cfg3a", "cfg3c"}  # thousands of streamed pieces: default and unstreamed only
 NAMES = ["cfg1A", "cfg1B", "cfg1C", "cfg1D", "cfg2e", "cfg2a", "cfg2b", "cfg2d", "cfg3b", "cfg3a",
          "cfg3c", "cfg4"]
@@ -107,7 +107,7 @@ def check_partition(w, plan, per_rank, world):
 
 
 def flag_sets(name):
-    return [0, 4096, 8192, 16384, 32769, 16789504, 1073745920] if name in HEAVY else FLAG_SETS
+    return [0, 4096, 8192, 16384, 32769, 16789504, 1073745920, 1610616832] if name in HEAVY else FLAG_SETS
 
 
 def _analyze_all(w, plan, world, flags):
