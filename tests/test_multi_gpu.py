@@ -89,8 +89,8 @@ def test_multi_gpu_parity(tmp_path, flags):
             print(f"rank {l['rank']}/{n} " + json.dumps({k: c.get(k) for k in ("case", "flags", "bad", "skipped",
                                                                             "nvlink_in", "nvlink_out", "streamed")
                                                       if k in c}))
-    for l in lines:
-        assert l["ok"], json.dumps(l)[:3000]
+    bad_ranks = [json.dumps(l)[:3000] for l in lines if not l["ok"]]
+    assert not bad_ranks, "\n".join(bad_ranks)
     # every byte pulled over NVLink by one rank is served by another
     for case in {c["case"] for c in lines[0]["cases"] if "case" in c}:
         for flags in {c["flags"] for c in lines[0]["cases"] if c.get("case") == case}:
