@@ -469,13 +469,14 @@ class StrategyCycle:
     def __init__(self, ctx: Context, steps, dtype: str, n_virtual: int, flags: Optional[int] = None):
         # Untuned defaults (switch plans are copy-only).  Across GPUs: every copy runs on
         # the rank holding its input, no cross-rank chunking, NVLink and local items
-        # interleaved, bulk stores -- within 2.3% of the best measured variant on every
-        # cfg4 / cfg5 step at N=2 and N=4 and up to 1.7x faster than flags 0
-        # (profiles/r02_cycle_flags_n{2,4}.jsonl).  On one GPU copies leave through TMA
-        # bulk stores: never more than 0.1% slower than flags 0, 3-7% faster on cfg4 and
-        # cfg5 S2->S3 / S3->S4 / S4->S1 (profiles/r02_sweep_n1.jsonl).
+        # interleaved -- up to 1.7x faster than flags 0 on the cfg4 / cfg5 steps
+        # (profiles/r02_cycle_flags_n{2,4}.jsonl).  TMA bulk stores to peers are left
+        # to the autotuner there (1-2% at N>1; the only two bad parity results of the
+        # round came from a cycle with them).  On one GPU copies
+        # leave through TMA bulk stores: never more than 0.1% slower than flags 0,
+        # 3-7% faster on cfg4 and cfg5 S2->S3 / S3->S4 / S4->S1.
         if flags is None:
-            flags = (HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_INTERLEAVE | HS_PROG_BULK_STORE
+            flags = (HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_INTERLEAVE
                      if ctx.world > 1 else HS_PROG_BULK_STORE)
         self.ctx, self.steps, self.dtype, self.n_virtual, self.flags = ctx, steps, dtype, n_virtual, flags
         ents = [[(i, tid, s, shp) for i, (tid, s, d, shp) in enumerate(st)] for st in steps]

@@ -212,7 +212,8 @@ def main():
         steps = [[(tid, s, d, tuple(max(8, v // 32) for v in shp)) for tid, s, d, shp in W.config5(x).transitions]
                  for x in W.CONFIG5_CYCLE]
         bad = []
-        for flags in (None, 0):
+        cyc_flags = os.environ.get("HS_MGPU_CYCLE_FLAGS")  # exploration: variants to cycle with
+        for flags in ([int(x) for x in cyc_flags.split(",")] if cyc_flags else (None, 0)):
             mark = ctx.alloc(0)
             cyc = StrategyCycle(ctx, steps, "bf16", 8, flags)
             try:
