@@ -224,9 +224,12 @@ def main():
                     prog, info = cyc.prepare(0)
                     if info["program_cached"] != (rnd == 1):
                         bad.append(("cache", flags, rnd))
+                    sync_prepare = os.environ.get("HS_MGPU_CYCLE_SYNC") == "1"  # exploration
                     for k in range(len(steps)):
+                        if sync_prepare and k > 0:
+                            prog = cyc.prepare(k)[0]
                         prog.run()  # enqueues only: the next step compiles meanwhile
-                        nxt = cyc.prepare(k + 1)[0] if k + 1 < len(steps) else None
+                        nxt = cyc.prepare(k + 1)[0] if k + 1 < len(steps) and not sync_prepare else None
                         ctx.sync()
                         dist.barrier()
                         b = cyc.states[k + 1].verify(7)
