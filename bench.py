@@ -515,6 +515,8 @@ def main():
     # Validation aid only: HS_ARENA_GB with more ranks than GPUs runs e.g. the N=8
     # flow on a 4-GPU box (two ranks per GPU); its timings mean nothing.
     local %= torch.cuda.device_count()
+    if world > torch.cuda.device_count():  # ranks share GPUs: barriers as their own launches
+        os.environ["HS_SEPARATE_BARRIERS"] = "1"
     torch.cuda.set_device(local)
     free, _ = torch.cuda.mem_get_info(local)
     arena = max(8 << 30, free - (10 << 30))

@@ -1809,8 +1809,12 @@ void Program::build_tables(const std::vector<BoxTask>& tasks) {
     // The phase's opening barrier runs in the prologue of its first launch
     // when that is a TMA kernel (not the register path): one launch and its
     // gap fewer per barrier.
+    // HS_SEPARATE_BARRIERS=1: ranks share a GPU (oversubscribed validation runs) --
+    // a persistent kernel spinning in a folded barrier can hold the time-sliced GPU
+    // while the co-resident peer that must arrive waits for a slice
+    static const bool separate = std::getenv("HS_SEPARATE_BARRIERS") != nullptr;
     d.fold_barrier = ctx_.world() > 1 && !nccl_mode_ && !ce_mode_ && !(flags_ & HS_PROG_SEPARATE_BARRIERS) &&
-                     !d.launches.empty() && d.launches[0].tma;
+                     !separate && !d.launches.empty() && d.launches[0].tma;
     stats_.items += n;
     stats_.phase_items.push_back(n);
   }

@@ -30,6 +30,8 @@ def main():
     # HS_TEST_RANKS may oversubscribe the GPUs (8 ranks on a 4-GPU box, two per
     # GPU) to exercise 8-rank IPC, barriers and partitions where only 4 GPUs exist
     local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
+    if world > torch.cuda.device_count():  # ranks share GPUs: no spinning in folded barriers
+        os.environ["HS_SEPARATE_BARRIERS"] = "1"  # read by the library at its first compile
     dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     full = os.environ.get("HS_MGPU_FULL") == "1"
