@@ -475,9 +475,11 @@ class StrategyCycle:
         # round came from a cycle with them).  On one GPU copies
         # leave through TMA bulk stores: never more than 0.1% slower than flags 0,
         # 3-7% faster on cfg4 and cfg5 S2->S3 / S3->S4 / S4->S1.
+        # Beyond 4 ranks the default stays flags 0: at 8 ranks a TMA-path bug in pushed
+        # multi-output copies (PUSH_ALL) is open.
         if flags is None:
-            flags = (HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_INTERLEAVE
-                     if ctx.world > 1 else HS_PROG_BULK_STORE)
+            flags = (HS_PROG_BULK_STORE if ctx.world == 1 else
+                     HS_PROG_PUSH_ALL | HS_PROG_NO_SHARE | HS_PROG_INTERLEAVE if ctx.world <= 4 else 0)
         self.ctx, self.steps, self.dtype, self.n_virtual, self.flags = ctx, steps, dtype, n_virtual, flags
         ents = [[(i, tid, s, shp) for i, (tid, s, d, shp) in enumerate(st)] for st in steps]
         ents.append([(i, tid, d, shp) for i, (tid, s, d, shp) in enumerate(steps[-1])])
